@@ -1,0 +1,80 @@
+"""Byte-ledger definition and closed forms (oracle).
+
+TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.
+
+The paper approximates communication volume as "total data received per device
+per iteration" and states that TawPipe "transfers a single weight shard and its
+corresponding gradients per step, totaling 24H²" (§3.5).
+§8(c) R14 and Appendix A turn that into integer per-device counters of LOGICAL
+elements (algorithm-independent):
+
+  all-gather of a G-striped vector  : each participant receives (G−1)s, sends (G−1)s
+  reduce-scatter of a G·s vector    : each participant receives (G−1)s, sends (G−1)s
+  P2P of x                          : receiver x, sender x
+
+Counter order (shared by this module, include/tawpipe.h and DESIGN.md):
+  index = ((kind·2 + cls)·2 + dir)·3 + unit
+  kind ∈ {0: weight, 1: grad}, cls ∈ {0: intra-group, 1: inter-group},
+  dir ∈ {0: received, 1: sent}, unit ∈ {0: decoder blocks, 1: E, 2: F}.
+"""
+from __future__ import annotations
+
+N_COUNTERS = 24
+KINDS = ("w", "g")
+CLASSES = ("intra", "inter")
+DIRS = ("recv", "sent")
+UNITS = ("block", "E", "F")
+
+
+def index(kind: str, cls: str, dir_: str, unit: str) -> int:
+    return ((KINDS.index(kind) * 2 + CLASSES.index(cls)) * 2 + DIRS.index(dir_)) * 3 + UNITS.index(unit)
+
+
+def name(i: int) -> str:
+    u = i % 3
+    d = (i // 3) % 2
+    c = (i // 6) % 2
+    k = i // 12
+    return f"{KINDS[k]}_{CLASSES[c]}_{DIRS[d]}_{UNITS[u]}"
+
+
+def closed_form(L: int, P: int, G: int, k: int, s: int, e: int, f: int, r: int = 1) -> list:
+    """SURVEY.md Appendix A, per device (k, j) per iteration, in elements.
+
+    L layers, P devices, G = devices per group, D = P/G groups, k = group index
+    of the device, s / e / f = stripe lengths of a decoder layer / E / F,
+    r = 1 when layer L−1's forward buffer is reused for its backward (R12).
+    """
+    D = P // G
+    assert P % G == 0 and L % D == 0
+    Lr = L * (D - 1) // D
+    out = [0] * N_COUNTERS
+
+    def put(kind, cls, dir_, unit, val):
+        out[index(kind, cls, dir_, unit)] = int(val)
+
+    # decoder blocks
+    put("w", "intra", "recv", "block", (2 * L - r) * (G - 1) * s)
+    put("w", "intra", "sent", "block", (2 * L - r) * (G - 1) * s)
+    put("w", "inter", "recv", "block", (2 * Lr - r * (1 if k != D - 1 else 0)) * s)
+    put("w", "inter", "sent", "block", (2 * (L // D) * (D - 1) - r * (D - 1) * (1 if k == D - 1 else 0)) * s)
+    put("g", "intra", "recv", "block", L * (G - 1) * s)
+    put("g", "intra", "sent", "block", L * (G - 1) * s)
+    put("g", "inter", "sent", "block", Lr * s)
+    put("g", "inter", "recv", "block", (L // D) * (D - 1) * s)
+    # pseudo-layers E (owner group 0) and F (owner group D−1): one gather, one reduction each
+    for unit, n, owner in (("E", e, 0), ("F", f, D - 1)):
+        put("w", "intra", "recv", unit, (G - 1) * n)
+        put("w", "intra", "sent", unit, (G - 1) * n)
+        put("w", "inter", "recv", unit, n if k != owner else 0)
+        put("w", "inter", "sent", unit, (D - 1) * n if k == owner else 0)
+        put("g", "intra", "recv", unit, (G - 1) * n)
+        put("g", "intra", "sent", unit, (G - 1) * n)
+        put("g", "inter", "sent", unit, n if k != owner else 0)
+        put("g", "inter", "recv", unit, (D - 1) * n if k == owner else 0)
+    return out
+
+
+def block_received(ledger: list) -> int:
+    """Total decoder-block elements received (weights + grads, intra + inter)."""
+    return sum(ledger[index(kd, c, "recv", "block")] for kd in KINDS for c in CLASSES)

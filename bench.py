@@ -1,0 +1,313 @@
+"""bench.py -- one TawPipe training step (GWPS + DBS + CCO) per timed iteration, B200, synthetic tokens.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    (N > 1: torchrun --nproc-per-node N ... ; RANK / WORLD_SIZE / LOCAL_RANK from the env)
+
+Metric (BASELINE.json): tokens/s for the LLaMA-style 7B at 32K context (C3: L=32, H=4096, n_h=32, I=11008,
+V=32000, S=32768, B=1, activation checkpointing, bf16, one 32,768-token micro-batch per GPU), D = N/G groups
+of G (4x2 at N=8, 2x2 at 4, 1x2 at 2, 1x1 at 1).  ``value`` is the whole-job tokens/s
+(max-over-ranks device time, CUDA events); ``e2e`` is the same through tawpipe_step with host tokens
+(H2D + loss D2H inside the timed region).  ``roofline`` is for the dominant kernel (GEMM: tensor bound),
+``cpu_baseline`` the fp64 oracle on the host cores (bounded sample, extrapolated to the workload).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s/GPU LLaMA-style 32K ctx at 1/2/4/8 B200; exposed comm ms/iter"
+
+# name -> (model, L, H, n_h, I, V, S, B, ckpt, tokens per GPU per step, group size by N)
+CONFIGS = {
+    "c0": dict(model="tiny", L=2, H=64, nh=4, I=192, V=256, S=128, B=1, ckpt=0, m=1, dtype=0,
+               groups={1: 1, 2: 2, 4: 2, 8: 2}),
+    "c0b": dict(model="tiny-bf16", L=2, H=256, nh=2, I=768, V=512, S=256, B=1, ckpt=0, m=1, dtype=1,
+                groups={1: 1, 2: 2, 4: 2, 8: 2}),
+    "c1": dict(model="llama-1.3B", L=24, H=2048, nh=16, I=5632, V=32000, S=8192, B=1, ckpt=0, m=4, dtype=1,
+               groups={1: 1, 2: 2, 4: 4, 8: 8}),
+    "c2": dict(model="llama-1.3B", L=24, H=2048, nh=16, I=5632, V=32000, S=16384, B=1, ckpt=0, m=2, dtype=1,
+               groups={1: 1, 2: 2, 4: 2, 8: 4}),
+    "c3": dict(model="llama-7B", L=32, H=4096, nh=32, I=11008, V=32000, S=32768, B=1, ckpt=1, m=1, dtype=1,
+               groups={1: 1, 2: 2, 4: 2, 8: 2}),
+    "c4": dict(model="llama-13B", L=40, H=5120, nh=40, I=13824, V=32000, S=16384, B=1, ckpt=1, m=2, dtype=1,
+               groups={1: 1, 2: 1, 4: 2, 8: 4}),
+}
+
+
+def flops_per_token(c, recompute=True):
+    """forward 2·φ_dense + 2H(S+1) per layer + 2HV head; train = 3×; + recompute."""
+    H, I, S, L, V = c["H"], c["I"], c["S"], c["L"], c["V"]
+    layer_fwd = 2 * (4 * H * H + 3 * H * I) + 2 * H * (S + 1)
+    f = 3 * (L * layer_fwd + 2 * H * V)
+    if recompute and c["ckpt"]:
+        f += L * layer_fwd
+    return f
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+            sm = [float(r[0]) for r in rows]
+            mx = [float(r[1]) for r in rows]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": reasons,
+                    "samples": len(sm)}
+        except Exception as e:  # no nvidia-smi / no samples
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": str(e)[:80]}
+
+
+# ------------------------------------------------------------------------------------------------ oracle
+def oracle_baseline(c, budget_s=20.0):
+    """The fp64 oracle (oracle/model.py) as it stands, on the host cores: one decoder layer at the workload's
+    full H and I on a bounded sequence sample (forward + recompute + backward + AdamW of that layer), then
+    extrapolated to the workload's tokens/s by FLOPs (SURVEY.md §8(d) "Oracle timing")."""
+    import numpy as np
+
+    import synth
+    from oracle import model as om
+    S = 256
+    while True:
+        cfg = om.ModelConfig(n_layers=1, hidden=c["H"], heads=c["nh"], ffn=c["I"], vocab=8, seq=S)
+        p = synth.init_params(1, c["H"], c["I"], 8)
+        P64 = om.to_f64(p)
+        W = P64["layers"][0]
+        cos, sin = om.rope_tables(S, cfg.head_dim, cfg.rope_theta)
+        h = np.random.default_rng(0).standard_normal((S, c["H"])) * 0.02
+        t0 = time.perf_counter()
+        _, cache = om.layer_fwd(h, W, cfg, cos, sin)          # forward
+        _, cache = om.layer_fwd(h, W, cfg, cos, sin)          # recompute (checkpointing)
+        _, g = om.layer_bwd(np.ones_like(h) * 1e-3, W, cache, cfg, cos, sin)
+        for k in om.LAYER_KEYS:
+            om.adamw_update(W[k], g[k], np.zeros_like(W[k]), np.zeros_like(W[k]), 1, cfg, True)
+        dt = time.perf_counter() - t0
+        if dt > budget_s / 4 or S >= 2048:
+            break
+        S *= 2
+    layer_fwd = 2 * (4 * c["H"] ** 2 + 3 * c["H"] * c["I"]) + 2 * c["H"] * (S + 1)
+    flops = S * layer_fwd * (4 if c["ckpt"] else 3)
+    fps = flops / dt
+    tok_s = fps / flops_per_token(c)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"one decoder layer (H={c['H']}, I={c['I']}) on S={S} tokens, fwd+recompute+bwd+AdamW "
+                      f"in {dt:.2f} s = {fps / 1e9:.1f} GFLOP/s fp64, extrapolated by FLOPs/token of the workload"}
+
+
+def run_reference(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = None
+    times = []
+    for i in range(args.warmup + args.steps):
+        cb = oracle_baseline(c, budget_s=max(5.0, 60.0 / max(1, args.steps + args.warmup)))
+        if i >= args.warmup:
+            times.append(cb["value"])
+    v = statistics.median(times)
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": config_name(args, c), "model": c["model"]},
+           "cpu_baseline": dict(cb, value=v),
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def config_name(args, c):
+    G = c["groups"].get(args.gpus, 1)
+    return (f"{args.config.upper()} {c['model']} L={c['L']} H={c['H']} S={c['S']} B={c['B']} "
+            f"ckpt={c['ckpt']} {args.gpus // G}x{G}")
+
+
+# ------------------------------------------------------------------------------------------------ ours
+def run_ours(args, c):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2511_09741_b200 import tawpipe as T
+
+    rank, world, local = T.dist_env()
+    assert world == args.gpus, f"WORLD_SIZE {world} != --gpus {args.gpus}"
+    torch.cuda.set_device(local)
+    T.bootstrap(rank, world, local, pg_backend="gloo")
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    G = c["groups"].get(world, 1)
+    N = c["m"] * world
+    dims = T.ModelDims(n_layers=c["L"], hidden=c["H"], heads=c["nh"], ffn=c["I"], vocab=c["V"], seq=c["S"],
+                       micro_bs=c["B"], dtype=c["dtype"], ckpt=c["ckpt"], lr=3e-4,
+                       schedule=T.NO_CCO if args.no_cco else T.GWPS)
+    verbose = bool(os.environ.get("TAWPIPE_BENCH_VERBOSE"))
+    if verbose:
+        import faulthandler
+        faulthandler.dump_traceback_later(90, repeat=True)
+    t_init = time.time()
+    sess = T.Session(world, G, dims, N)
+    sess.set_timing(True)
+    if verbose:
+        print(f"[rank {rank}] init {time.time() - t_init:.1f} s, {sess.stats()['alloc_gb']:.1f} GB", file=sys.stderr,
+              flush=True)
+    tok_host = [synth.tokens(N, c["B"], c["S"], c["V"], step=s) for s in range(2)]
+    mine = [np.ascontiguousarray(t[rank * c["m"]:(rank + 1) * c["m"]]) for t in tok_host]
+    tok_dev = [torch.from_numpy(x).cuda() for x in mine]
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(args.warmup):
+        t0 = time.time()
+        loss = sess.step_device(tok_dev[i % 2].data_ptr())
+        if verbose:
+            print(f"[rank {rank}] warmup step {i}: loss {loss:.4f} {time.time() - t0:.2f} s "
+                  f"{ {k: round(v, 2) for k, v in sess.stats().items()} }", file=sys.stderr, flush=True)
+    barrier()
+    torch.cuda.synchronize()
+    stats_acc = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for i in range(args.steps):
+            loss = sess.step_device(tok_dev[i % 2].data_ptr())
+            stats_acc.append(sess.stats())
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        # e2e: host tokens, H2D of this rank's slice + loss D2H inside tawpipe_step
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        n_e2e = max(1, min(args.steps, 2))
+        for i in range(n_e2e):
+            loss_e2e = sess.step(tok_host[i % 2])
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / n_e2e)
+    tokens_step = N * c["B"] * c["S"]
+    st = {k: statistics.mean(s[k] for s in stats_acc) for k in stats_acc[0]}
+    exposed = max_over_ranks(st["exposed_comm_ms"])
+    ledger = sess.ledger()
+    peaks, peak_src = load_peaks()
+    # dominant kernel by device time: GEMM (tensor) or attention (tensor)
+    gemm_tf = st["gemm_gflop"] / max(st["gemm_ms"], 1e-9)  # GFLOP/ms == TFLOP/s
+    attn_tf = st["attn_gflop"] / max(st["attn_ms"], 1e-9)
+    if st["gemm_ms"] >= st["attn_ms"]:
+        dom, ach, dom_ms = "tcgen05 GEMM (all dense contractions of the step)", gemm_tf, st["gemm_ms"]
+    else:
+        dom, ach, dom_ms = "causal attention fwd+bwd", attn_tf, st["attn_ms"]
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    wire = 2 if c["dtype"] == 1 else 4
+    step_roof_ms = max(flops_per_token(c) * c["m"] * c["B"] * c["S"] / (peaks["bf16_tflops"] * 1e12) * 1e3,
+                       max(sum(ledger[i] for i in range(24) if (i // 3) % 2 == 0),
+                           sum(ledger[i] for i in range(24) if (i // 3) % 2 == 1)) * wire / 770e9 * 1e3)
+    out = {
+        "metric": METRIC, "value": tokens_step / (ms / 1e3), "unit": "tokens/s",
+        "tokens_per_s_per_gpu": tokens_step / (ms / 1e3) / world,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if c["dtype"] else "f32",
+        "data": "synthetic (uniform tokens, seeded device init N(0,0.02))",
+        "config": {"workload": config_name(args, c), "model": c["model"], "global_batch": N * c["B"],
+                   "seq_len": c["S"], "parallelism": f"tawpipe {world // G}x{G} (D x G)",
+                   "l2": "inputs and weights far larger than L2 (no flush needed)",
+                   "schedule": "no-CCO ablation" if args.no_cco else "GWPS+DBS+CCO"},
+        "exposed_comm_ms": exposed, "exposed_comm_frac": exposed / ms,
+        "step_roofline_frac": step_roof_ms / ms,
+        "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                     "frac": ach / peak, "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "share_of_step": dom_ms / ms},
+        "kernel_ms": {"gemm": st["gemm_ms"], "attention": st["attn_ms"], "adamw": st["adamw_ms"],
+                      "elementwise": st["elementwise_ms"]},
+        "gpu_launches": int(round(st["kernel_launches"] * args.steps)),
+        "e2e": {"value": tokens_step / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(mine[0].nbytes), "d2h_bytes_per_step": 8},
+        "loss": loss, "loss_e2e": loss_e2e,
+        "clocks": clk.summary(),
+        "ledger_elems": ledger,
+        "alloc_gb": st["alloc_gb"],
+    }
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            try:
+                out["cpu_baseline"] = oracle_baseline(c, budget_s=20.0)
+            except Exception as e:
+                out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(out), flush=True)
+    sess.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cco", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, c)
+    else:
+        run_ours(args, c)
+
+
+if __name__ == "__main__":
+    main()

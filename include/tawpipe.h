@@ -1,0 +1,173 @@
+/*
+ * tawpipe.h -- C ABI of the B200-native TawPipe training-step library (libtawpipe.so).
+ *
+ * What the library computes.  One synchronous training iteration of a LLaMA-style
+ * decoder under TawPipe's three mechanisms (§3.1):
+ *   - DBS, device-bound storage: every layer's weights, gradients and optimizer state are
+ *     statically bound to devices (§3.2).  Reading R6: layer l is
+ *     owned by group l mod D and striped G ways over the group's members.
+ *   - GWPS, group-based weight pipeline scheduling: devices form D contiguous groups of G
+ *     (§3.3); weights move by intra-group all-gather and inter-group rail P2P,
+ *     gradients by intra-group reduce-scatter and rail P2P to the owner.
+ *   - CCO, communication-computation overlap: layer l+1 is prefetched on a side stream
+ *     while layer l computes (§3.4).
+ * The result equals one step of plain single-device mini-batch AdamW on all N·B sequences
+ * (SURVEY.md §8(c)); parity is checked against the fp64 oracle in oracle/.
+ *
+ * Process model.  SPMD, one process per GPU, one live context per process.  Calls marked
+ * COLLECTIVE must be made by every rank in the same order.  Calls are not thread-safe.
+ *
+ * Errors.  Functions returning int return TAWPIPE_OK (0) or a negative code; tawpipe_step
+ * returns NaN on error.  tawpipe_last_error() describes the last failure.  After any error
+ * other than TAWPIPE_ECONFIG the context is unusable until tawpipe_finalize().
+ *
+ * There is no CPU fallback: every step of the path runs in this library's CUDA kernels.
+ */
+#ifndef TAWPIPE_H_
+#define TAWPIPE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TAWPIPE_OK          0
+#define TAWPIPE_ECONFIG    -2   /* invalid configuration / argument (SPEC.md:515 exit code 2)        */
+#define TAWPIPE_EINVARIANT -3   /* internal invariant failure (SPEC.md:515 exit code 3)              */
+#define TAWPIPE_ERUNTIME   -4   /* CUDA or NCCL runtime error (SPEC.md:515 exit code 4)              */
+#define TAWPIPE_EUNINIT    -5   /* call before tawpipe_bootstrap / tawpipe_init                       */
+
+#define TAWPIPE_FP32 0          /* parity path: every tensor, wire and accumulator fp32 (SIMT FMA)    */
+#define TAWPIPE_BF16 1          /* bf16 weights/activations/wire, fp32 accumulation/master/m/v        */
+
+/* schedule flags (tawpipe_dims.schedule) */
+#define TAWPIPE_GWPS   0        /* default: the paper's schedule                                     */
+#define TAWPIPE_NO_CCO 1        /* ablation: gather of layer l+1 waits for compute of l */
+
+#define TAWPIPE_LEDGER_N 24     /* see tawpipe_ledger */
+#define TAWPIPE_STATS_N  16     /* see tawpipe_stats  */
+
+/* Model dimensions and hyper-parameters.  Symbols follow PAPER.md Table 1;
+ * the rest are LLaMA-2 conventions. */
+typedef struct tawpipe_dims {
+  int32_t hidden;        /* H                                                                   */
+  int32_t heads;         /* n_h; head dim d_h = H / n_h                                          */
+  int32_t ffn;           /* I, SwiGLU width                                                      */
+  int32_t vocab;         /* V                                                                    */
+  int32_t seq;           /* S, tokens per sequence fed to the model                              */
+  int32_t micro_bs;      /* B, sequences per micro-batch                                          */
+  int32_t dtype;         /* TAWPIPE_FP32 | TAWPIPE_BF16                                          */
+  int32_t ckpt;          /* 1: keep only each layer's input h_l, recompute in backward */
+  int32_t schedule;      /* TAWPIPE_GWPS | TAWPIPE_NO_CCO                                        */
+  int32_t reserved;      /* must be 0                                                            */
+  float lr, beta1, beta2, adam_eps, weight_decay;   /* AdamW, torch semantics (R1)               */
+  float rms_eps, rope_theta;                        /* 1e-5, 10000 (R10)                          */
+  uint64_t seed;         /* device-side N(0,0.02) init when tawpipe_load is not called (R20)    */
+} tawpipe_dims;
+
+/* Create an NCCL unique id (128 bytes) on the calling rank (rank 0 of the job).  LOCAL.
+ * out: caller-owned buffer of >= 128 bytes.  Returns 0 or TAWPIPE_ERUNTIME. */
+int tawpipe_get_unique_id(void* out);
+
+/* Bind this process to `device` and, when world > 1, create the world NCCL communicator from
+ * `unique_id` (128 bytes from tawpipe_get_unique_id on rank 0, distributed by the caller --
+ * the Python binding uses torch.distributed for that).  COLLECTIVE when world > 1.
+ * unique_id may be NULL when world == 1. */
+int tawpipe_bootstrap(int rank, int world, int device, const void* unique_id);
+
+/* Build the DBS plan and allocate all device state.  COLLECTIVE.
+ *   n_devices  P; must equal the bootstrap world size.
+ *   group_size G = P / D; P mod G == 0 ("P mod D = 0").
+ *   n_layers   L; L mod D == 0 (reading R6 replaces the paper's L mod P = 0).
+ *   dims       model dimensions (copied).
+ *   n_micro    N micro-batches per iteration, N mod P == 0; each device takes m = N/P
+ *              contiguous micro-batches (R4).
+ * bf16 path shape limits: d_h in {64,128}, S mod 128 == 0, H, I, V multiples of 128.
+ * Weights are initialised on the device from dims->seed; call tawpipe_load to override.
+ * Returns 0, TAWPIPE_ECONFIG (message names the violated constraint) or TAWPIPE_ERUNTIME. */
+int tawpipe_init(int n_devices, int group_size, int n_layers, const tawpipe_dims* dims, int n_micro);
+
+/* Load the full model (host fp32, canonical layout, n_elems = V·H + L·φ + H + V·H with
+ * φ = 4H²+3HI+2H): [E | layer 0 .. layer L−1 | γ_f | W_head], each layer
+ * [attn_norm | Wq | Wk | Wv | Wo | mlp_norm | Wgate | Wup | Wdown], matrices row-major
+ * [out, in].  Each rank keeps only its owned stripes; resets AdamW state and step count.
+ * COLLECTIVE (no communication, but every rank must call it). */
+int tawpipe_load(const float* full_model_fp32, int64_t n_elems);
+
+/* One training iteration.  tokens: host int32 [N][B][S+1], identical on every rank; inputs are
+ * positions 0..S−1 and targets 1..S of each sequence (R3).  The library copies this rank's
+ * micro-batches to the device inside the call.  Returns the global mean loss over N·B·S
+ * predicted tokens (R2), identical on all ranks, after every AdamW of the step has completed
+ * (synchronous).  NaN on error.  COLLECTIVE. */
+float tawpipe_step(const int32_t* tokens);
+
+/* Same as tawpipe_step but `dev_tokens` is this rank's own slice, already resident in device
+ * memory: int32 [m][B][S+1] with m = N/P.  Used to time the step with inputs in HBM. */
+float tawpipe_step_device(const int32_t* dev_tokens);
+
+/* Number of fp32 elements tawpipe_shard writes on this rank.  LOCAL. */
+int64_t tawpipe_shard_elems(void);
+
+/* Copy this rank's owned fp32 master stripes to host memory `out` (caller-owned, >=
+ * tawpipe_shard_elems() floats), canonical order: owned decoder layers ascending, then E (if
+ * owned), then F (if owned); for each unit, the stripe [j·s, (j+1)·s) of its zero-padded
+ * flat vector (padding to G·64·ceil(n/(G·64)) elements).  Returns elements written or < 0. LOCAL. */
+int64_t tawpipe_shard(float* out);
+
+/* Byte ledger of the last step (logical elements): out[i] for
+ * i = ((kind·2 + cls)·2 + dir)·3 + unit, kind {0 weight, 1 grad}, cls {0 intra-group,
+ * 1 inter-group}, dir {0 received, 1 sent}, unit {0 decoder blocks, 1 E, 2 F}.
+ * n >= TAWPIPE_LEDGER_N.  Bytes = elements × wire size (2 bf16, 4 fp32).  LOCAL. */
+int tawpipe_ledger(uint64_t* out, int n);
+
+/* Timing of the last step (requires tawpipe_set_timing(1) before it), n >= TAWPIPE_STATS_N:
+ *  [0] step ms (compute stream, event to event)      [1] exposed-comm ms (compute-stream waits)
+ *  [2] weight-comm ms (wstream busy)                 [3] grad-comm+AdamW ms (gstream busy)
+ *  [4] GEMM ms (sum of tcgen05/SIMT GEMM launches)   [5] GEMM algorithmic GFLOP
+ *  [6] GEMM launches                                 [7] attention ms   [8] attention GFLOP
+ *  [9] AdamW ms   [10] AdamW algorithmic GB          [11] kernel launches in the step
+ *  [12] peak device bytes allocated (GB)             [13] wire bytes per element
+ *  [14] elementwise/norm ms                          [15] reserved                        LOCAL. */
+int tawpipe_stats(double* out, int n);
+
+/* Enable (1) / disable (0) per-kernel CUDA-event timing for tawpipe_stats.  LOCAL. */
+int tawpipe_set_timing(int on);
+
+/* Thread-local description of the last error (never NULL).  LOCAL. */
+const char* tawpipe_last_error(void);
+
+/* Free all device memory and communicators.  COLLECTIVE when world > 1. */
+void tawpipe_finalize(void);
+
+/* ---- kernel-level entry points (used by the per-op parity tests; device pointers) ---- */
+
+/* C[M,N] (+)= Σ_k A(m,k)·B(n,k) on `stream` (cudaStream_t, NULL = legacy default).
+ * A(m,k) = A[m·a_ld + k] if a_kmajor else A[k·a_ld + m]; likewise B(n,k).
+ * dtype: TAWPIPE_BF16 (bf16 A/B, tcgen05, fp32 accumulate in TMEM) or TAWPIPE_FP32 (SIMT).
+ * c_f32: C is fp32 (else the dtype); accumulate: C += result (else C = result);
+ * R (nullable, same dtype/ld as C): C = R + result.  bf16 shape limits: M mod 128, N mod 128,
+ * K mod 64 == 0, 16-byte aligned pointers and leading dimensions. */
+int tawpipe_gemm(int dtype, int64_t M, int64_t N, int64_t K,
+                 const void* A, int64_t a_ld, int a_kmajor,
+                 const void* B, int64_t b_ld, int b_kmajor,
+                 void* C, int64_t c_ld, int c_f32, int accumulate,
+                 const void* R, void* stream);
+
+/* Causal attention forward on one micro-batch: qkv [B·S, 3H] (q | k | v column blocks,
+ * head h at columns h·d_h of each block, RoPE already applied), o [B·S, H], lse fp32 [B][n_h][S]
+ * (natural log).  dtype as above. */
+int tawpipe_attention_fwd(int dtype, int B, int S, int n_h, int d_h,
+                          const void* qkv, void* o, float* lse, void* stream);
+
+/* Causal attention backward: do_ [B·S, H] -> dqkv [B·S, 3H] (dq | dk | dv, w.r.t. the roped q,k).
+ * `delta` is fp32 scratch of B·n_h·S floats; `dq_acc` fp32 scratch of B·S·H floats (may be NULL
+ * for the fp32 path). */
+int tawpipe_attention_bwd(int dtype, int B, int S, int n_h, int d_h,
+                          const void* qkv, const void* o, const float* lse, const void* do_,
+                          void* dqkv, float* delta, float* dq_acc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAWPIPE_H_ */

@@ -1,0 +1,564 @@
+// attn_tc.cu -- causal flash attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Computes the causal softmax attention of SURVEY.md §8(c) step 2 (and its backward, §8(c) table) for the
+// bf16 path, one (128-row tile, head, sequence) per CTA:
+//   forward : S = Q·Kᵀ (TMEM) -> online softmax in registers (exp2, lazily rescaled running max) ->
+//             P (bf16, smem) -> O += P·V (TMEM); O / l and LSE written at the end.
+//   backward: per 128-row key tile: Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ (TMEM) -> Pᵀ = exp(Sᵀ − LSE), dSᵀ = Pᵀ⊙(dPᵀ − δ)
+//             (bf16, smem) -> dV += Pᵀ·dO, dK += dSᵀ·Q (TMEM, persistent), dQ_i = dS·K (TMEM) reduced into an
+//             fp32 accumulator with vector atomics; δ = rowsum(dO⊙O) comes from a pre-pass.
+// Causal tiles above the diagonal are skipped (the masked half is work the method avoids, App. B).
+// Operand tiles are loaded once by TMA (128 rows × 64 columns, 128-byte swizzle); the same smem tile serves
+// as a K-major operand (Q, K for QKᵀ) and as an MN-major operand (V, dO, Q, K in the PV / gradient products).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace tp {
+
+CUtensorMap make_tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer);
+
+namespace {
+
+constexpr int BQ = 128;       // rows per tile (queries or keys)
+constexpr int ATOM = 16384;   // one 128-row × 64-col bf16 SW128 tile
+constexpr float LOG2E = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// write one 128-element fp32 row as bf16 into a K-major SW128 tile pair (2 atoms of 64 columns)
+__device__ __forceinline__ void store_row_sw128(uint8_t* tile, int r, const float* v) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      uint4 o;
+      const float* x = v + a * 64 + c * 8;
+      o.x = pack_bf16(x[0], x[1]);
+      o.y = pack_bf16(x[2], x[3]);
+      o.z = pack_bf16(x[4], x[5]);
+      o.w = pack_bf16(x[6], x[7]);
+      *reinterpret_cast<uint4*>(tile + a * ATOM + r * 128 + ((c ^ (r & 7)) << 4)) = o;
+    }
+  }
+}
+
+// K-major SW128 descriptor for k-slice ks (16 elements) of a tile made of 64-column atoms
+__device__ __forceinline__ uint64_t desc_k(uint32_t base, int ks) {
+  return umma_desc_sw128(base + (ks >> 2) * ATOM + (ks & 3) * 32, 16, 1024);
+}
+// MN-major view of the same storage: K runs over rows (16 rows per slice), MN atoms 16 KB apart
+__device__ __forceinline__ uint64_t desc_mn(uint32_t base, int ks) {
+  return umma_desc_sw128(base + ks * 2048, ATOM, 1024);
+}
+
+// =============================================================================================== forward
+template <int DH>
+struct FwdSmem {
+  static constexpr int QB = DH / 64 * ATOM;  // Q / K / V tile bytes
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = QB;           // 2 stages
+  static constexpr int OFF_V = 3 * QB;       // 2 stages
+  static constexpr int OFF_P = 5 * QB;       // 2 atoms
+  static constexpr int OFF_BAR = OFF_P + 2 * ATOM;
+  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(192, 1)
+    fa_fwd_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
+                  int nh, float scale2) {
+  using L = FwdSmem<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
+           *s_full = bar + 9, *p_full = bar + 11, *o_done = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int n_q = S / BQ;
+  const int qt = n_q - 1 - static_cast<int>(blockIdx.x / nh);  // heaviest tiles first
+  const int h = blockIdx.x % nh;
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int n_kv = qt + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 128};
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, L::QB);
+      for (int a = 0; a < DH / 64; ++a)
+        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qt * BQ);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
+                      row0 + j * BQ);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
+      const uint32_t sQ = smem_u32(sm + L::OFF_Q), sP = smem_u32(sm + L::OFF_P);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS[st], desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (n_kv > 1) issue_s(1);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tO, desc_k(sP, ks), desc_mn(sV, ks), id_pv, (j | ks) > 0);
+        umma_commit(&v_empty[st]);
+        umma_commit(o_done);
+        if (j + 2 < n_kv) issue_s(j + 2);
+      }
+    }
+  } else {
+    // softmax warps: thread t <-> query row t of the tile (TMEM lane t)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* sP = sm + L::OFF_P;
+    float m2 = -INFINITY, l = 0.f;
+    float s[128];
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tS[st] + lane_off + c * 32, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]) * scale2;
+      }
+      if (j == qt) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > r) s[i] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} done: O stable, P buffer free
+      tc_fence_after();
+      if (j == 0) {
+        m2 = mx;
+      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
+        // lazy rescale (the stale max bounds P by 2^8); tcgen05.ld/st are warp-collective, so the whole warp
+        // rescales together, each row by its own factor (1 when its max did not grow)
+        const float mnew = fmaxf(m2, mx);
+        const float alpha = ex2(m2 - mnew);
+        l *= alpha;
+#pragma unroll 1
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld32(tO + lane_off + c * 32, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st32(tO + lane_off + c * 32, u);
+        }
+        tmem_wait_st();
+        m2 = mnew;
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        const float p = ex2(s[i] - m2);
+        s[i] = p;
+        sum += p;
+      }
+      l += sum;
+      store_row_sw128(sP, r, s);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(o_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tO + lane_off + c * 32, u);
+      tmem_wait_ld();
+      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 o;
+        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+        d4[v] = o;
+      }
+    }
+    lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// =============================================================================================== backward
+template <int DH>
+struct BwdSmem {
+  static constexpr int QB = DH / 64 * ATOM;
+  static constexpr int OFF_K = 0, OFF_V = QB, OFF_Q = 2 * QB, OFF_DO = 3 * QB;
+  static constexpr int OFF_P = 4 * QB;           // Pᵀ  [kv][q], 2 atoms
+  static constexpr int OFF_DS = OFF_P + 2 * ATOM;  // dSᵀ [kv][q], 2 atoms
+  static constexpr int OFF_LSE = OFF_DS + 2 * ATOM;  // 2 × 128 floats (double-buffered)
+  static constexpr int OFF_DEL = OFF_LSE + 1024;
+  static constexpr int OFF_BAR = OFF_DEL + 1024;
+  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(192, 1)
+    fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
+                  const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
+                  bf16* __restrict__ dqkv, int S, int nh, float scale, float scale2) {
+  using L = BwdSmem<DH>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 2, *s_full = bar + 3, *dp_full = bar + 4,
+           *ds_full = bar + 5, *mma2_done = bar + 6, *dq_free = bar + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
+  float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
+
+  const int n_q = S / BQ;
+  const int jt = static_cast<int>(blockIdx.x / nh);  // heaviest key tiles (most query tiles) first
+  const int h = blockIdx.x % nh;
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int n_it = n_q - jt;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tm);
+    tma_prefetch(&tmdo);
+    mbar_init(kv_full, 1);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 128);
+    mbar_init(mma2_done, 1);
+    mbar_init(dq_free, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * L::QB);
+      for (int a = 0; a < DH / 64; ++a) {
+        tma_load_2d(sm + L::OFF_K + a * ATOM, &tm, kv_full, H + h * DH + a * 64, row0 + jt * BQ);
+        tma_load_2d(sm + L::OFF_V + a * ATOM, &tm, kv_full, 2 * H + h * DH + a * 64, row0 + jt * BQ);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int i = jt + it;
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_expect_tx(q_full, 2 * L::QB);
+        for (int a = 0; a < DH / 64; ++a) {
+          tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + i * BQ);
+          tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, q_full, h * DH + a * 64, row0 + i * BQ);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);    // Sᵀ, dPᵀ: K-major A and B (K = d)
+      constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);     // dV, dK: A K-major (K = q), B MN-major
+      constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);       // dQ: A = dSᵀ viewed MN-major, B MN-major
+      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sQ = smem_u32(sm + L::OFF_Q),
+                     sDO = smem_u32(sm + L::OFF_DO), sP = smem_u32(sm + L::OFF_P), sDS = smem_u32(sm + L::OFF_DS);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        mbar_wait(q_full, it & 1);
+        if (it > 0) mbar_wait(dq_free, (it - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
+        umma_commit(s_full);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
+        umma_commit(dp_full);
+        mbar_wait(ds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) {
+          umma_f16(tdV, desc_k(sP, ks), desc_mn(sDO, ks), id_kv, (it | ks) > 0);
+          umma_f16(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
+        }
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tS, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
+        umma_commit(q_empty);
+        umma_commit(mma2_done);
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int t = q * 32 + lane;   // TMEM lane: key row (Sᵀ, dPᵀ, dK, dV) or query row (dQ)
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* sP = sm + L::OFF_P;
+    uint8_t* sDS = sm + L::OFF_DS;
+    float p[128];
+    for (int it = 0; it < n_it; ++it) {
+      const int i = jt + it;
+      const int buf = it & 1;
+      const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ + t;
+      lse_s[buf * 128 + t] = lse[li] * LOG2E;
+      del_s[buf * 128 + t] = delta[li];
+      named_bar(1, 128);
+      const float* ls = lse_s + buf * 128;
+      const float* ds_ = del_s + buf * 128;
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tS + lane_off + c * 32, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) p[c * 32 + k] = ex2(__uint_as_float(u[k]) * scale2 - ls[c * 32 + k]);
+      }
+      if (it == 0) {  // diagonal tile: query index < key index is masked
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if (k < t) p[k] = 0.f;
+      }
+      if (it > 0) mbar_wait(mma2_done, (it - 1) & 1);  // Pᵀ / dSᵀ smem of the previous iteration consumed
+      store_row_sw128(sP, t, p);
+      mbar_wait(dp_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tdP + lane_off + c * 32, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) p[c * 32 + k] = p[c * 32 + k] * (__uint_as_float(u[k]) - ds_[c * 32 + k]);
+      }
+      store_row_sw128(sDS, t, p);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+      // dQ_i rows (TMEM lane = query row t of tile i) -> fp32 accumulator
+      mbar_wait(mma2_done, it & 1);
+      tc_fence_after();
+      float* dq = dq_acc + static_cast<int64_t>(row0 + i * BQ + t) * H + h * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tS + lane_off + c * 32, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 32 + v * 4),
+                       "f"(__uint_as_float(u[4 * v])), "f"(__uint_as_float(u[4 * v + 1])),
+                       "f"(__uint_as_float(u[4 * v + 2])), "f"(__uint_as_float(u[4 * v + 3]))
+                       : "memory");
+      }
+      tc_fence_before();
+      mbar_arrive(dq_free);
+    }
+    // dK (× softmax scale) and dV rows of this key tile
+    mbar_wait(mma2_done, (n_it - 1) & 1);
+    tc_fence_after();
+    bf16* dk = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + H + h * DH;
+    bf16* dv = dk + H;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32], w[32];
+      tmem_ld32(tdK + lane_off + c * 32, u);
+      tmem_ld32(tdV + lane_off + c * 32, w);
+      tmem_wait_ld();
+      uint4* k4 = reinterpret_cast<uint4*>(dk + c * 32);
+      uint4* v4 = reinterpret_cast<uint4*>(dv + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 o, o2;
+        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * scale, __uint_as_float(u[8 * v + 1]) * scale);
+        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * scale, __uint_as_float(u[8 * v + 3]) * scale);
+        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * scale, __uint_as_float(u[8 * v + 5]) * scale);
+        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * scale, __uint_as_float(u[8 * v + 7]) * scale);
+        o2.x = pack_bf16(__uint_as_float(w[8 * v + 0]), __uint_as_float(w[8 * v + 1]));
+        o2.y = pack_bf16(__uint_as_float(w[8 * v + 2]), __uint_as_float(w[8 * v + 3]));
+        o2.z = pack_bf16(__uint_as_float(w[8 * v + 4]), __uint_as_float(w[8 * v + 5]));
+        o2.w = pack_bf16(__uint_as_float(w[8 * v + 6]), __uint_as_float(w[8 * v + 7]));
+        k4[v] = o;
+        v4[v] = o2;
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// δ_i = Σ_d dO_id·O_id ; one warp per (row, head)
+__global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16* __restrict__ o,
+                                const bf16* __restrict__ dout, float* __restrict__ delta) {
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= rows * nh) return;
+  const int64_t row = w / nh;
+  const int h = static_cast<int>(w % nh);
+  const int H = nh * dh;
+  float acc = 0.f;
+  for (int d = lane * 2; d < dh; d += 64) {
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(o + row * H + h * dh + d);
+    const __nv_bfloat162 c = *reinterpret_cast<const __nv_bfloat162*>(dout + row * H + h * dh + d);
+    acc += __bfloat162float(a.x) * __bfloat162float(c.x) + __bfloat162float(a.y) * __bfloat162float(c.y);
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) delta[(row / S * nh + h) * S + row % S] = acc;
+}
+
+// dq (bf16, × softmax scale) <- fp32 accumulator
+__global__ void fa_dq_convert_kernel(int64_t rows, int H, const float* __restrict__ acc, bf16* __restrict__ dqkv,
+                                     float scale) {
+  const int64_t n = rows * H / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(acc)[i];
+    const int64_t e = i * 4;
+    const int64_t r = e / H, c = e % H;
+    uint2 o;
+    o.x = pack_bf16(v.x * scale, v.y * scale);
+    o.y = pack_bf16(v.z * scale, v.w * scale);
+    *reinterpret_cast<uint2*>(dqkv + r * 3 * H + c) = o;
+  }
+}
+
+template <typename K>
+void prep(K kern, int bytes) {
+  TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+}  // namespace
+
+bool attention_tc_supported(int S, int dh) { return S % 128 == 0 && (dh == 64 || dh == 128); }
+
+void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, float* lse, cudaStream_t s) {
+  TP_CHECK(attention_tc_supported(S, dh), TAWPIPE_ECONFIG, "tcgen05 attention: S % 128 == 0, d_h in {64, 128}");
+  const int H = nh * dh;
+  CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, static_cast<int64_t>(B) * S, 3ll * H, 128);
+  const float scale2 = LOG2E / sqrtf(static_cast<float>(dh));
+  dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+  if (dh == 128) {
+    static bool once = (prep(fa_fwd_kernel<128>, FwdSmem<128>::BYTES), true);
+    (void)once;
+    fa_fwd_kernel<128><<<grid, 192, FwdSmem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+  } else {
+    static bool once = (prep(fa_fwd_kernel<64>, FwdSmem<64>::BYTES), true);
+    (void)once;
+    fa_fwd_kernel<64><<<grid, 192, FwdSmem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+  }
+  TP_CUDA(cudaGetLastError());
+  g_kstats.launches++;
+}
+
+void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16* o, const float* lse,
+                      const bf16* dout, bf16* dqkv, float* delta, float* dq_acc, cudaStream_t s) {
+  TP_CHECK(attention_tc_supported(S, dh), TAWPIPE_ECONFIG, "tcgen05 attention: S % 128 == 0, d_h in {64, 128}");
+  TP_CHECK(dq_acc != nullptr, TAWPIPE_ECONFIG, "tcgen05 attention backward needs the fp32 dq accumulator");
+  const int H = nh * dh;
+  const int64_t rows = static_cast<int64_t>(B) * S;
+  fa_delta_kernel<<<static_cast<unsigned>((rows * nh * 32 + 255) / 256), 256, 0, s>>>(rows, S, nh, dh, o, dout,
+                                                                                    delta);
+  TP_CUDA(cudaMemsetAsync(dq_acc, 0, rows * H * sizeof(float), s));
+  CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, rows, 3ll * H, 128);
+  CUtensorMap tmdo = make_tmap_bf16_2d(dout, H, rows, H, 128);
+  const float scale = 1.0f / sqrtf(static_cast<float>(dh));
+  const float scale2 = LOG2E * scale;
+  dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+  if (dh == 128) {
+    static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
+    (void)once;
+    fa_bwd_kernel<128><<<grid, 192, BwdSmem<128>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
+                                                               scale2);
+  } else {
+    static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
+    (void)once;
+    fa_bwd_kernel<64><<<grid, 192, BwdSmem<64>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
+                                                             scale2);
+  }
+  fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
+  TP_CUDA(cudaGetLastError());
+  g_kstats.launches += 3;
+}
+
+}  // namespace tp

@@ -1,0 +1,125 @@
+// common.cuh -- shared declarations of libtawpipe's CUDA sources.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "tawpipe.h"
+
+namespace tp {
+
+using bf16 = __nv_bfloat16;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define TP_CUDA(x)                                                                                        \
+  do {                                                                                                    \
+    cudaError_t e_ = (x);                                                                                 \
+    if (e_ != cudaSuccess)                                                                                \
+      throw ::tp::Error(TAWPIPE_ERUNTIME, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " +       \
+                                              __FILE__ + ":" + std::to_string(__LINE__) + " (" #x ")"); \
+  } while (0)
+
+#define TP_CHECK(cond, code, msg)                       \
+  do {                                                  \
+    if (!(cond)) throw ::tp::Error((code), (msg));      \
+  } while (0)
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<bf16>(bf16 x) { return __bfloat162float(x); }
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// ---------------------------------------------------------------- launch accounting
+struct KernelStats {
+  long launches = 0;
+};
+extern KernelStats g_kstats;
+
+// ---------------------------------------------------------------- GEMM (gemm_tc.cu / gemm_simt.cu)
+struct GemmArgs {
+  int64_t M, N, K;
+  const void* A;
+  int64_t lda;
+  bool a_kmajor;
+  const void* B;
+  int64_t ldb;
+  bool b_kmajor;
+  void* C;
+  int64_t ldc;
+  bool c_f32;
+  bool accumulate;
+  const void* R;  // residual (same dtype / ld as C), nullable
+};
+void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s);   // tcgen05 + TMA + TMEM
+template <typename T>
+void gemm_simt(const GemmArgs& g, cudaStream_t s);      // generic strided SIMT (fp32 parity path)
+
+// ---------------------------------------------------------------- attention (attn_*.cu)
+template <typename T>
+void attention_fwd_simt(int B, int S, int nh, int dh, const T* qkv, T* o, float* lse, cudaStream_t s);
+template <typename T>
+void attention_bwd_simt(int B, int S, int nh, int dh, const T* qkv, const T* o, const float* lse, const T* dout,
+                        T* dqkv, float* delta, cudaStream_t s);
+void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, float* lse, cudaStream_t s);
+void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16* o, const float* lse,
+                      const bf16* dout, bf16* dqkv, float* delta, float* dq_acc, cudaStream_t s);
+bool attention_tc_supported(int S, int dh);
+
+// ---------------------------------------------------------------- elementwise / norm / loss / optimizer
+template <typename T>
+void embed_fwd(const int32_t* tok, int64_t tok_stride_seq, int B, int S, const T* E, int H, T* h, cudaStream_t s);
+void embed_bwd(const int32_t* tok, int64_t tok_stride_seq, int B, int S, const void* dh, bool dh_f32, int H,
+               float* dE, cudaStream_t s);
+template <typename T>
+void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s);
+// dx = (res ? res : 0) + RMSNorm'(dy); dg_acc += Σ_rows dy⊙x⊙r (fp32)
+template <typename T>
+void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
+                 int64_t rows, int H, cudaStream_t s);
+template <typename T>
+void rope_apply(T* qkv, int B, int S, int nh, int dh, const float* cos, const float* sin, bool inverse, int ncols_blocks,
+                cudaStream_t s);
+template <typename T>
+void swiglu_fwd(const T* gu, T* y, int64_t rows, int I, cudaStream_t s);
+template <typename T>
+void swiglu_bwd(const T* dy, const T* gu, T* dgu, int64_t rows, int I, cudaStream_t s);
+// logits [rows, V] in place -> dz; loss_rows[r] = LSE - z[t]
+template <typename T>
+void cross_entropy(T* logits, const int32_t* targets, int64_t rows, int V, float inv_denom, float* loss_rows,
+                   cudaStream_t s);
+void sum_f32_to_f64(const float* x, int64_t n, double* out_accum, cudaStream_t s);
+template <typename T>
+void cast_f32(const float* x, T* y, int64_t n, cudaStream_t s);
+template <typename T>
+void cast_to_f32(const T* x, float* y, int64_t n, cudaStream_t s);
+template <typename T>
+void init_normal(T* wire, float* master, int64_t n, int64_t global_off, uint64_t seed, float std, cudaStream_t s);
+void fill_f32(float* x, int64_t n, float v, cudaStream_t s);
+
+struct AdamParams {
+  float lr, beta1, beta2, eps, wd;
+  float bc1, bc2;  // 1 - beta^t
+};
+// Sum the D group contributions (ascending k; contribution own_k may be fp32) and apply AdamW
+// to the owned stripe [off, off+n) of a unit whose no-decay ranges are nd[0..n_nd).
+template <typename W>
+void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_f32, float* master, float* m,
+                 float* v, W* wire, int64_t n, int64_t unit_off, const int64_t* nd_lo, const int64_t* nd_hi,
+                 int n_nd, AdamParams p, cudaStream_t s);
+
+}  // namespace tp

@@ -1,0 +1,1078 @@
+// engine.cu -- DBS plan, GWPS/CCO step engine and the C ABI of libtawpipe.
+//
+// Paper mapping (§3; readings R1-R21 in SURVEY.md §8(c), listed in DESIGN.md):
+//   DBS      : layer l is owned by group l mod D, striped over its G members (R6); each rank keeps
+//                             fp32 master / m / v and a wire-dtype copy of its owned stripes only.
+//   GWPS : per layer, rail P2P of stripe j from the owner group (inter-group, "wp"), then an
+//                             intra-group all-gather ("wb"); gradients are reduce-scattered in the group ("gr")
+//                             and sent on the rail to the owner ("gp"), which sums the D group contributions in
+//                             ascending group order and applies AdamW locally (R16).
+//   CCO : gathers run on a weight stream (ws) one layer ahead of the compute stream (cs),
+//                             into double-buffered layer slots; gradient reduction + AdamW run on a third stream (gs).
+// Every step of the path runs in this library's kernels; torch only bootstraps the process group (no CPU fallback).
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace tp {
+
+#define TP_NCCL(x)                                                                                             \
+  do {                                                                                                         \
+    ncclResult_t r_ = (x);                                                                                     \
+    if (r_ != ncclSuccess)                                                                                     \
+      throw ::tp::Error(TAWPIPE_ERUNTIME, std::string("NCCL: ") + ncclGetErrorString(r_) + " at " + __FILE__ + \
+                                              ":" + std::to_string(__LINE__));                                 \
+  } while (0)
+
+namespace {
+
+enum { U_BLOCK = 0, U_E = 1, U_F = 2 };
+enum { K_W = 0, K_G = 1 };
+enum { C_INTRA = 0, C_INTER = 1 };
+enum { D_RECV = 0, D_SENT = 1 };
+inline int ledger_index(int kind, int cls, int dir, int unit) { return ((kind * 2 + cls) * 2 + dir) * 3 + unit; }
+
+struct Unit {
+  int cls = U_BLOCK;
+  int64_t n = 0, n_pad = 0, s = 0;  // elements, padded, stripe
+  int owner = 0;                    // owner group
+  bool owned = false;
+  int64_t off = 0;                  // offset of this rank's stripe in the owned-state arrays
+  int64_t canon = 0;                // offset of the unit in the canonical full-model vector
+  int n_nd = 0;
+  int64_t nd_lo[2] = {0, 0}, nd_hi[2] = {0, 0};  // no-decay ranges (unit coordinates)
+};
+
+struct Acts {  // one (layer, micro-batch) forward's saved tensors
+  void *a, *qkv, *o, *h1, *b, *gu, *y;
+  float *r1, *lse, *r2;
+};
+
+struct TimedRegion {
+  cudaEvent_t a, b;
+  int kind;  // 0 gemm, 1 attention, 2 adamw, 3 exposed wait, 4 elementwise
+  double work;
+};
+
+struct Ctx {
+  // process / topology
+  int rank = 0, world = 1, device = 0;
+  bool booted = false, inited = false;
+  ncclComm_t world_comm = nullptr;
+  int P = 1, G = 1, D = 1, k = 0, j = 0, L = 0, N = 1, m = 1;
+  tawpipe_dims dims{};
+  int H = 0, nh = 0, dh = 0, I = 0, V = 0, S = 0, Bm = 1;
+  int64_t T = 0, phi = 0;
+  bool bf = false;
+  size_t esz = 4;
+  ncclComm_t wg = nullptr, wr = nullptr, gg = nullptr, gr = nullptr;
+  cudaStream_t cs = nullptr, ws = nullptr, gs = nullptr;
+  std::vector<Unit> units;  // 0..L-1 layers, L = E, L+1 = F
+  int64_t owned_total = 0, max_pad = 0, max_s = 0;
+  float *master = nullptr, *mom = nullptr, *vel = nullptr;
+  void* wire = nullptr;
+  void* wbuf[2] = {nullptr, nullptr};
+  void *ebuf = nullptr, *fbuf = nullptr;
+  float* gacc[2] = {nullptr, nullptr};
+  float *gaccE = nullptr, *gaccF = nullptr;
+  void *gwire = nullptr, *rsout = nullptr, *crecv = nullptr;
+  // activations
+  std::vector<void*> ck;  // (L+1) * m  residual-stream checkpoints h_l
+  std::vector<Acts> acts;  // L*m (no ckpt) or 1 (ckpt)
+  std::vector<void*> dhb;  // m: gradient of the residual stream per micro-batch
+  void *dY = nullptr, *dGU = nullptr, *db = nullptr, *dh1 = nullptr, *dO = nullptr, *dqkv = nullptr, *da = nullptr;
+  float *delta = nullptr, *dq_acc = nullptr;
+  void *fnorm = nullptr, *logits = nullptr, *df = nullptr;
+  float *rstd_f = nullptr, *loss_rows = nullptr;
+  int64_t Tc = 0;
+  int32_t *d_tok = nullptr, *d_in = nullptr, *d_tgt = nullptr, *h_tok = nullptr;
+  float *cosT = nullptr, *sinT = nullptr;
+  double* d_loss = nullptr;
+  double* h_loss = nullptr;
+  uint64_t ledger[TAWPIPE_LEDGER_N] = {};
+  int step_t = 0;
+  // events
+  cudaEvent_t w_ready[2], w_free[2], g_ready[2], g_free[2], evE, evF, evGF, evGE, ev_s0, ev_s1, ev_ws0, ev_ws1,
+      ev_gs0, ev_gs1;
+  // timing
+  bool timing = false;
+  std::vector<TimedRegion> regions;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  double stats[TAWPIPE_STATS_N] = {};
+  size_t bytes_alloc = 0;
+  std::vector<void*> allocs;
+  long launches_at_start = 0;
+};
+
+Ctx* g = nullptr;
+thread_local std::string g_err = "no error";
+
+void* dmalloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 256;
+  TP_CUDA(cudaMalloc(&p, bytes));
+  g->allocs.push_back(p);
+  g->bytes_alloc += bytes;
+  return p;
+}
+
+cudaEvent_t pool_event() {
+  if (g->ev_used == g->ev_pool.size()) {
+    cudaEvent_t e;
+    TP_CUDA(cudaEventCreate(&e));
+    g->ev_pool.push_back(e);
+  }
+  return g->ev_pool[g->ev_used++];
+}
+
+bool trace_on() {
+  static const bool on = std::getenv("TAWPIPE_TRACE") != nullptr;
+  return on;
+}
+#define TRACE(...)                                 \
+  do {                                             \
+    if (trace_on()) {                              \
+      std::fprintf(stderr, "[tawpipe] " __VA_ARGS__); \
+      std::fflush(stderr);                         \
+    }                                              \
+  } while (0)
+
+struct Timed {  // RAII CUDA-event bracket on a stream (only when timing is enabled)
+  cudaStream_t s;
+  TimedRegion r{};
+  bool on;
+  Timed(cudaStream_t st, int kind, double work) : s(st), on(g->timing) {
+    if (trace_on()) {
+      TP_CUDA(cudaDeviceSynchronize());
+      TRACE("region kind %d work %.3g start\n", kind, work);
+    }
+    if (!on) return;
+    r.a = pool_event();
+    r.b = pool_event();
+    r.kind = kind;
+    r.work = work;
+    TP_CUDA(cudaEventRecord(r.a, s));
+  }
+  ~Timed() noexcept(false) {
+    if (trace_on()) {
+      TP_CUDA(cudaDeviceSynchronize());
+      TRACE("region kind %d done\n", r.kind);
+    }
+    if (!on) return;
+    TP_CUDA(cudaEventRecord(r.b, s));
+    g->regions.push_back(r);
+  }
+};
+
+inline ncclDataType_t wire_type() { return g->bf ? ncclBfloat16 : ncclFloat32; }
+inline char* wptr(void* base, int64_t elems) { return static_cast<char*>(base) + elems * static_cast<int64_t>(g->esz); }
+
+// ------------------------------------------------------------------------------------ kernel dispatch
+void gemm(int64_t M, int64_t Nn, int64_t K, const void* A, int64_t lda, bool akm, const void* B, int64_t ldb, bool bkm,
+          void* C, int64_t ldc, bool c_f32, bool acc, const void* R, cudaStream_t s) {
+  GemmArgs a{M, Nn, K, A, lda, akm, B, ldb, bkm, C, ldc, c_f32, acc, R};
+  Timed t(s, 0, 2.0 * M * Nn * K);
+  static const bool force_simt = [] {
+    const char* e = std::getenv("TAWPIPE_GEMM");
+    return e && std::string(e) == "simt";
+  }();
+  if (!g->bf)
+    gemm_simt<float>(a, s);
+  else if (force_simt)
+    gemm_simt<bf16>(a, s);
+  else
+    gemm_tc_bf16(a, s);
+}
+
+bool use_tc_attention() {
+  static const int mode = [] {
+    const char* e = std::getenv("TAWPIPE_ATTN");
+    if (e && std::string(e) == "simt") return 0;
+    return 1;
+  }();
+  return g->bf && mode == 1 && attention_tc_supported(g->S, g->dh);
+}
+
+double attn_flops_fwd() {  // causal: QKᵀ and PV each H·S(S+1) MACs per sequence -> 2·2·H·S(S+1)/2·... (App. B)
+  return 2.0 * g->H * (g->S + 1.0) * g->S * g->Bm;
+}
+
+void attn_fwd(const void* qkv, void* o, float* lse, cudaStream_t s) {
+  Timed t(s, 1, attn_flops_fwd());
+  if (!g->bf)
+    attention_fwd_simt<float>(g->Bm, g->S, g->nh, g->dh, (const float*)qkv, (float*)o, lse, s);
+  else if (use_tc_attention())
+    attention_fwd_tc(g->Bm, g->S, g->nh, g->dh, (const bf16*)qkv, (bf16*)o, lse, s);
+  else
+    attention_fwd_simt<bf16>(g->Bm, g->S, g->nh, g->dh, (const bf16*)qkv, (bf16*)o, lse, s);
+}
+void attn_bwd(const void* qkv, const void* o, const float* lse, const void* dout, void* dqkv, cudaStream_t s) {
+  Timed t(s, 1, 2.0 * attn_flops_fwd());
+  if (!g->bf)
+    attention_bwd_simt<float>(g->Bm, g->S, g->nh, g->dh, (const float*)qkv, (const float*)o, lse, (const float*)dout,
+                              (float*)dqkv, g->delta, s);
+  else if (use_tc_attention())
+    attention_bwd_tc(g->Bm, g->S, g->nh, g->dh, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)dout,
+                     (bf16*)dqkv, g->delta, g->dq_acc, s);
+  else
+    attention_bwd_simt<bf16>(g->Bm, g->S, g->nh, g->dh, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)dout,
+                             (bf16*)dqkv, g->delta, s);
+}
+
+#define BY_TYPE(call_f32, call_bf16) \
+  do {                               \
+    if (g->bf) {                     \
+      call_bf16;                     \
+    } else {                         \
+      call_f32;                      \
+    }                                \
+  } while (0)
+
+void k_rmsnorm_fwd(const void* x, const void* gm, void* y, float* r, int64_t rows, cudaStream_t s) {
+  Timed t(s, 4, 0);
+  BY_TYPE(rmsnorm_fwd<float>((const float*)x, (const float*)gm, (float*)y, r, rows, g->H, g->dims.rms_eps, s),
+          rmsnorm_fwd<bf16>((const bf16*)x, (const bf16*)gm, (bf16*)y, r, rows, g->H, g->dims.rms_eps, s));
+}
+void k_rmsnorm_bwd(const void* dy, const void* x, const void* gm, const float* r, const void* res, void* dx,
+                   float* dgacc, int64_t rows, cudaStream_t s) {
+  Timed t(s, 4, 0);
+  BY_TYPE(rmsnorm_bwd<float>((const float*)dy, (const float*)x, (const float*)gm, r, (const float*)res, (float*)dx,
+                             dgacc, rows, g->H, s),
+          rmsnorm_bwd<bf16>((const bf16*)dy, (const bf16*)x, (const bf16*)gm, r, (const bf16*)res, (bf16*)dx, dgacc,
+                            rows, g->H, s));
+}
+void k_rope(void* qkv, bool inverse, cudaStream_t s) {
+  Timed t(s, 4, 0);
+  BY_TYPE(rope_apply<float>((float*)qkv, g->Bm, g->S, g->nh, g->dh, g->cosT, g->sinT, inverse, 2, s),
+          rope_apply<bf16>((bf16*)qkv, g->Bm, g->S, g->nh, g->dh, g->cosT, g->sinT, inverse, 2, s));
+}
+
+// ------------------------------------------------------------------------------------ comm (a3, a8)
+void ledger_add(int kind, int cls, int dir, int unit, int64_t n) {
+  g->ledger[ledger_index(kind, cls, dir, unit)] += static_cast<uint64_t>(n);
+}
+
+// full unit buffer the compute reads for unit u (slot for layers)
+void* unit_buffer(int uid, int slot) {
+  const Unit& u = g->units[uid];
+  if (g->G == 1 && u.owned) return wptr(g->wire, u.off);
+  if (u.cls == U_E) return g->ebuf;
+  if (u.cls == U_F) return g->fbuf;
+  return g->wbuf[slot];
+}
+
+// a3: rail P2P of stripe j from the owner group (if remote) + intra-group all-gather, on ws
+void gather(int uid, void* dst) {
+  const Unit& u = g->units[uid];
+  if (g->G == 1 && u.owned) return;
+  Timed t(g->ws, 5, 0);
+  void* own = wptr(g->wire, u.off);
+  if (g->D > 1) {
+    TP_NCCL(ncclGroupStart());
+    if (u.owned) {
+      for (int kk = 0; kk < g->D; ++kk)
+        if (kk != g->k) TP_NCCL(ncclSend(own, u.s, wire_type(), kk, g->wr, g->ws));
+      ledger_add(K_W, C_INTER, D_SENT, u.cls, u.s * (g->D - 1));
+    } else {
+      TP_NCCL(ncclRecv(wptr(dst, g->j * u.s), u.s, wire_type(), u.owner, g->wr, g->ws));
+      ledger_add(K_W, C_INTER, D_RECV, u.cls, u.s);
+    }
+    TP_NCCL(ncclGroupEnd());
+  }
+  if (g->G > 1) {
+    const void* send = u.owned ? own : wptr(dst, g->j * u.s);
+    TP_NCCL(ncclAllGather(send, dst, u.s, wire_type(), g->wg, g->ws));
+    ledger_add(K_W, C_INTRA, D_RECV, u.cls, u.s * (g->G - 1));
+    ledger_add(K_W, C_INTRA, D_SENT, u.cls, u.s * (g->G - 1));
+  }
+}
+
+// a8 + a9: reduce-scatter in the group, rail P2P to the owner, ascending-k accumulate + AdamW, on gs
+void reduce_and_update(int uid, float* gacc) {
+  const Unit& u = g->units[uid];
+  cudaStream_t s = g->gs;
+  const void* own_partial = gacc;
+  bool own_f32 = true;
+  if (g->G > 1 || (g->D > 1 && !u.owned)) {
+    Timed t(s, 4, 0);
+    BY_TYPE(cast_f32<float>(gacc, (float*)g->gwire, u.n_pad, s), cast_f32<bf16>(gacc, (bf16*)g->gwire, u.n_pad, s));
+    own_partial = g->gwire;
+    own_f32 = false;
+  }
+  if (g->G > 1) {
+    Timed t(s, 5, 0);
+    TP_NCCL(ncclReduceScatter(g->gwire, g->rsout, u.s, wire_type(), ncclSum, g->gg, s));
+    ledger_add(K_G, C_INTRA, D_RECV, u.cls, u.s * (g->G - 1));
+    ledger_add(K_G, C_INTRA, D_SENT, u.cls, u.s * (g->G - 1));
+    own_partial = g->rsout;
+  }
+  if (g->D > 1) {
+    Timed t(s, 5, 0);
+    TP_NCCL(ncclGroupStart());
+    if (u.owned) {
+      int idx = 0;
+      for (int kk = 0; kk < g->D; ++kk)
+        if (kk != g->k) TP_NCCL(ncclRecv(wptr(g->crecv, (idx++) * u.s), u.s, wire_type(), kk, g->gr, s));
+      ledger_add(K_G, C_INTER, D_RECV, u.cls, u.s * (g->D - 1));
+    } else {
+      TP_NCCL(ncclSend(own_partial, u.s, wire_type(), u.owner, g->gr, s));
+      ledger_add(K_G, C_INTER, D_SENT, u.cls, u.s);
+    }
+    TP_NCCL(ncclGroupEnd());
+  }
+  if (!u.owned) return;
+  const void* contrib[8];
+  int idx = 0;
+  for (int kk = 0; kk < g->D; ++kk) contrib[kk] = (kk == g->k) ? own_partial : wptr(g->crecv, (idx++) * u.s);
+  AdamParams hp;
+  hp.lr = g->dims.lr;
+  hp.beta1 = g->dims.beta1;
+  hp.beta2 = g->dims.beta2;
+  hp.eps = g->dims.adam_eps;
+  hp.wd = g->dims.weight_decay;
+  hp.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta1), g->step_t));
+  hp.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta2), g->step_t));
+  const int64_t stripe_off = static_cast<int64_t>(g->j) * u.s;
+  Timed t(s, 2, (2.0 * g->D * g->esz + 26.0) * u.s);
+  BY_TYPE(adamw_fused<float>(contrib, g->D, g->k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
+                             (float*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s),
+          adamw_fused<bf16>(contrib, g->D, g->k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
+                            (bf16*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s));
+}
+
+void wait_on(cudaStream_t s, cudaEvent_t e) {
+  if (s == g->cs && g->timing) {
+    Timed t(s, 3, 0);
+    TP_CUDA(cudaStreamWaitEvent(s, e, 0));
+  } else {
+    TP_CUDA(cudaStreamWaitEvent(s, e, 0));
+  }
+}
+
+// ------------------------------------------------------------------------------------ layer compute (a5, a7)
+struct LayerW {
+  const void *attn_norm, *wqkv, *wo, *mlp_norm, *wgu, *wdown;
+};
+LayerW layer_weights(void* W) {
+  const int64_t H = g->H, I = g->I;
+  LayerW w;
+  w.attn_norm = wptr(W, 0);
+  w.wqkv = wptr(W, H);
+  w.wo = wptr(W, H + 3 * H * H);
+  w.mlp_norm = wptr(W, H + 4 * H * H);
+  w.wgu = wptr(W, 2 * H + 4 * H * H);
+  w.wdown = wptr(W, 2 * H + 4 * H * H + 2 * I * H);
+  return w;
+}
+
+Acts& acts_for(int l, int mb) { return g->dims.ckpt ? g->acts[0] : g->acts[static_cast<size_t>(l) * g->m + mb]; }
+void* ck(int l, int mb) { return g->ck[static_cast<size_t>(l) * g->m + mb]; }
+
+void layer_forward(int l, int mb, void* W, bool write_out) {
+  cudaStream_t s = g->cs;
+  const int64_t T = g->T, H = g->H, I = g->I;
+  LayerW w = layer_weights(W);
+  Acts& A = acts_for(l, mb);
+  void* hin = ck(l, mb);
+  k_rmsnorm_fwd(hin, w.attn_norm, A.a, A.r1, T, s);
+  gemm(T, 3 * H, H, A.a, H, true, w.wqkv, H, true, A.qkv, 3 * H, false, false, nullptr, s);
+  k_rope(A.qkv, false, s);
+  attn_fwd(A.qkv, A.o, A.lse, s);
+  gemm(T, H, H, A.o, H, true, w.wo, H, true, A.h1, H, false, false, hin, s);
+  k_rmsnorm_fwd(A.h1, w.mlp_norm, A.b, A.r2, T, s);
+  gemm(T, 2 * I, H, A.b, H, true, w.wgu, H, true, A.gu, 2 * I, false, false, nullptr, s);
+  {
+    Timed t(s, 4, 0);
+    BY_TYPE(swiglu_fwd<float>((const float*)A.gu, (float*)A.y, T, (int)I, s),
+            swiglu_fwd<bf16>((const bf16*)A.gu, (bf16*)A.y, T, (int)I, s));
+  }
+  if (write_out) gemm(T, H, I, A.y, I, true, w.wdown, I, true, ck(l + 1, mb), H, false, false, A.h1, s);
+}
+
+void layer_backward(int l, int mb, void* W, float* G_) {
+  cudaStream_t s = g->cs;
+  const int64_t T = g->T, H = g->H, I = g->I;
+  LayerW w = layer_weights(W);
+  if (g->dims.ckpt) layer_forward(l, mb, W, false);  // recompute from the checkpoint h_l
+  Acts& A = acts_for(l, mb);
+  void* hin = ck(l, mb);
+  void* dh = g->dhb[mb];
+  float* gq = G_ + H;                      // Wq|Wk|Wv  [3H, H]
+  float* go = G_ + H + 3 * H * H;          // Wo        [H, H]
+  float* gmn = G_ + H + 4 * H * H;         // mlp_norm  [H]
+  float* ggu = G_ + 2 * H + 4 * H * H;     // Wgate|Wup [2I, H]
+  float* gd = G_ + 2 * H + 4 * H * H + 2 * I * H;  // Wdown [H, I]
+  // h2 = h1 + y·Wdownᵀ
+  gemm(H, I, T, dh, H, false, A.y, I, false, gd, I, true, true, nullptr, s);
+  gemm(T, I, H, dh, H, true, w.wdown, I, false, g->dY, I, false, false, nullptr, s);
+  {
+    Timed t(s, 4, 0);
+    BY_TYPE(swiglu_bwd<float>((const float*)g->dY, (const float*)A.gu, (float*)g->dGU, T, (int)I, s),
+            swiglu_bwd<bf16>((const bf16*)g->dY, (const bf16*)A.gu, (bf16*)g->dGU, T, (int)I, s));
+  }
+  gemm(2 * I, H, T, g->dGU, 2 * I, false, A.b, H, false, ggu, H, true, true, nullptr, s);
+  gemm(T, H, 2 * I, g->dGU, 2 * I, true, w.wgu, H, false, g->db, H, false, false, nullptr, s);
+  k_rmsnorm_bwd(g->db, A.h1, w.mlp_norm, A.r2, dh, g->dh1, gmn, T, s);
+  // h1 = h + o·Woᵀ
+  gemm(H, H, T, g->dh1, H, false, A.o, H, false, go, H, true, true, nullptr, s);
+  gemm(T, H, H, g->dh1, H, true, w.wo, H, false, g->dO, H, false, false, nullptr, s);
+  attn_bwd(A.qkv, A.o, A.lse, g->dO, g->dqkv, s);
+  k_rope(g->dqkv, true, s);
+  gemm(3 * H, H, T, g->dqkv, 3 * H, false, A.a, H, false, gq, H, true, true, nullptr, s);
+  gemm(T, H, 3 * H, g->dqkv, 3 * H, true, w.wqkv, H, false, g->da, H, false, false, nullptr, s);
+  k_rmsnorm_bwd(g->da, hin, w.attn_norm, A.r1, g->dh1, dh, G_, T, s);
+}
+
+// a6: final RMSNorm + LM head + cross-entropy, forward and backward back to back, in row chunks
+void head(int mb, void* F, float* GF) {
+  cudaStream_t s = g->cs;
+  const int64_t T = g->T, H = g->H, V = g->V;
+  const void* gf = F;
+  const void* Wh = wptr(F, H);
+  void* hL = ck(g->L, mb);
+  k_rmsnorm_fwd(hL, gf, g->fnorm, g->rstd_f, T, s);
+  const float inv_denom = 1.0f / static_cast<float>(static_cast<double>(g->N) * g->Bm * g->S);
+  for (int64_t c0 = 0; c0 < T; c0 += g->Tc) {
+    const int64_t tc = (T - c0) < g->Tc ? (T - c0) : g->Tc;
+    void* fc = wptr(g->fnorm, c0 * H);
+    gemm(tc, V, H, fc, H, true, Wh, H, true, g->logits, V, false, false, nullptr, s);
+    {
+      Timed t(s, 4, 0);
+      const int32_t* tg = g->d_tgt + static_cast<int64_t>(mb) * T + c0;
+      BY_TYPE(cross_entropy<float>((float*)g->logits, tg, tc, (int)V, inv_denom, g->loss_rows + c0, s),
+              cross_entropy<bf16>((bf16*)g->logits, tg, tc, (int)V, inv_denom, g->loss_rows + c0, s));
+    }
+    gemm(V, H, tc, g->logits, V, false, fc, H, false, GF + H, H, true, true, nullptr, s);
+    gemm(tc, H, V, g->logits, V, true, Wh, H, false, wptr(g->df, c0 * H), H, false, false, nullptr, s);
+  }
+  k_rmsnorm_bwd(g->df, hL, gf, g->rstd_f, nullptr, g->dhb[mb], GF, T, s);
+  sum_f32_to_f64(g->loss_rows, T, g->d_loss, s);
+}
+
+__global__ void split_tokens_kernel(const int32_t* __restrict__ tok, int64_t seqs, int S, int32_t* __restrict__ in,
+                                    int32_t* __restrict__ tgt) {
+  const int64_t n = seqs * S;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t q = i / S, p = i % S;
+    in[i] = tok[q * (S + 1) + p];
+    tgt[i] = tok[q * (S + 1) + p + 1];
+  }
+}
+
+// ------------------------------------------------------------------------------------ one iteration
+double run_step(const int32_t* tokens, bool device_tokens) {
+  Ctx& c = *g;
+  c.step_t += 1;
+  std::memset(c.ledger, 0, sizeof(c.ledger));
+  c.regions.clear();
+  c.ev_used = 0;
+  c.launches_at_start = g_kstats.launches;
+  const int64_t seqs = static_cast<int64_t>(c.m) * c.Bm;
+  const int64_t tok_elems = seqs * (c.S + 1);
+  TRACE("step %d begin (device tokens %d)\n", c.step_t, device_tokens ? 1 : 0);
+  TP_CUDA(cudaEventRecord(c.ev_s0, c.cs));
+  TP_CUDA(cudaEventRecord(c.ev_ws0, c.ws));
+  TP_CUDA(cudaEventRecord(c.ev_gs0, c.gs));
+  if (device_tokens) {
+    TP_CUDA(cudaMemcpyAsync(c.d_tok, tokens, tok_elems * 4, cudaMemcpyDeviceToDevice, c.cs));
+  } else {
+    const int32_t* mine = tokens + static_cast<int64_t>(c.rank) * tok_elems;  // contiguous m micro-batches (R4)
+    std::memcpy(c.h_tok, mine, tok_elems * 4);
+    TP_CUDA(cudaMemcpyAsync(c.d_tok, c.h_tok, tok_elems * 4, cudaMemcpyHostToDevice, c.cs));
+  }
+  split_tokens_kernel<<<256, 256, 0, c.cs>>>(c.d_tok, seqs, c.S, c.d_in, c.d_tgt);
+  TP_CUDA(cudaGetLastError());
+  g_kstats.launches++;
+  TP_CUDA(cudaMemsetAsync(c.d_loss, 0, sizeof(double), c.cs));
+  if (trace_on()) {
+    TP_CUDA(cudaDeviceSynchronize());
+    TRACE("tokens staged\n");
+  }
+  const bool cco = !(c.dims.schedule & TAWPIPE_NO_CCO);
+  const int E = c.L, F = c.L + 1;
+  // ws / gs start after cs has seen the tokens (keeps all three streams inside the timed step)
+  TP_CUDA(cudaEventRecord(c.evGE, c.cs));
+  TP_CUDA(cudaStreamWaitEvent(c.ws, c.evGE, 0));
+  TP_CUDA(cudaStreamWaitEvent(c.gs, c.evGE, 0));
+
+  // ---- E: gather (forward only), embed (a4)
+  void* Ebuf = unit_buffer(E, 0);
+  gather(E, Ebuf);
+  TP_CUDA(cudaEventRecord(c.evE, c.ws));
+  wait_on(c.cs, c.evE);
+  for (int mb = 0; mb < c.m; ++mb) {
+    Timed t(c.cs, 4, 0);
+    BY_TYPE(embed_fwd<float>(c.d_in + static_cast<int64_t>(mb) * c.T, c.S, c.Bm, c.S, (const float*)Ebuf, c.H,
+                             (float*)ck(0, mb), c.cs),
+            embed_fwd<bf16>(c.d_in + static_cast<int64_t>(mb) * c.T, c.S, c.Bm, c.S, (const bf16*)Ebuf, c.H,
+                            (bf16*)ck(0, mb), c.cs));
+  }
+  // ---- forward with CCO prefetch (a3, a5)
+  gather(0, unit_buffer(0, 0));
+  TP_CUDA(cudaEventRecord(c.w_ready[0], c.ws));
+  for (int l = 0; l < c.L; ++l) {
+    const int slot = l & 1;
+    if (cco && l + 1 < c.L) {
+      TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[(l + 1) & 1], 0));
+      gather(l + 1, unit_buffer(l + 1, (l + 1) & 1));
+      TP_CUDA(cudaEventRecord(c.w_ready[(l + 1) & 1], c.ws));
+    }
+    if (l == c.L - 1) {  // F lives in its own buffer: prefetch it during the last layer
+      gather(F, unit_buffer(F, 0));
+      TP_CUDA(cudaEventRecord(c.evF, c.ws));
+    }
+    wait_on(c.cs, c.w_ready[slot]);
+    void* W = unit_buffer(l, slot);
+    TRACE("forward layer %d\n", l);
+    for (int mb = 0; mb < c.m; ++mb) layer_forward(l, mb, W, true);
+    TP_CUDA(cudaEventRecord(c.w_free[slot], c.cs));
+    if (!cco && l + 1 < c.L) {  // ablation: transfer serialised after the compute of the current step
+      TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[slot], 0));
+      gather(l + 1, unit_buffer(l + 1, (l + 1) & 1));
+      TP_CUDA(cudaEventRecord(c.w_ready[(l + 1) & 1], c.ws));
+    }
+  }
+  // ---- head F (a6)
+  wait_on(c.cs, c.evF);
+  TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.units[F].n_pad * 4, c.cs));
+  void* Fbuf = unit_buffer(F, 0);
+  for (int mb = 0; mb < c.m; ++mb) head(mb, Fbuf, c.gaccF);
+  TP_CUDA(cudaEventRecord(c.evGF, c.cs));
+  wait_on(c.gs, c.evGF);
+  reduce_and_update(F, c.gaccF);
+  // ---- backward (a7) with prefetch of l-1, gradient reduction + AdamW on gs (a8, a9)
+  for (int l = c.L - 1; l >= 0; --l) {
+    const int slot = l & 1;
+    if (cco && l - 1 >= 0) {
+      TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[(l - 1) & 1], 0));
+      gather(l - 1, unit_buffer(l - 1, (l - 1) & 1));
+      TP_CUDA(cudaEventRecord(c.w_ready[(l - 1) & 1], c.ws));
+    }
+    if (l != c.L - 1) wait_on(c.cs, c.w_ready[slot]);  // r = 1: layer L-1 reuses its forward buffer (R12)
+    wait_on(c.cs, c.g_free[slot]);
+    TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.units[l].n_pad * 4, c.cs));
+    void* W = unit_buffer(l, slot);
+    TRACE("backward layer %d\n", l);
+    for (int mb = 0; mb < c.m; ++mb) layer_backward(l, mb, W, c.gacc[slot]);
+    TP_CUDA(cudaEventRecord(c.w_free[slot], c.cs));
+    TP_CUDA(cudaEventRecord(c.g_ready[slot], c.cs));
+    if (!cco && l - 1 >= 0) {
+      TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[slot], 0));
+      gather(l - 1, unit_buffer(l - 1, (l - 1) & 1));
+      TP_CUDA(cudaEventRecord(c.w_ready[(l - 1) & 1], c.ws));
+    }
+    TP_CUDA(cudaStreamWaitEvent(c.gs, c.g_ready[slot], 0));
+    reduce_and_update(l, c.gacc[slot]);
+    TP_CUDA(cudaEventRecord(c.g_free[slot], c.gs));
+  }
+  // ---- E backward: scatter-add into the fp32 accumulator, then reduce + update (a4, a8, a9)
+  TP_CUDA(cudaMemsetAsync(c.gaccE, 0, c.units[E].n_pad * 4, c.cs));
+  for (int mb = 0; mb < c.m; ++mb) {
+    Timed t(c.cs, 4, 0);
+    embed_bwd(c.d_in + static_cast<int64_t>(mb) * c.T, c.S, c.Bm, c.S, c.dhb[mb], !c.bf, c.H, c.gaccE, c.cs);
+  }
+  TP_CUDA(cudaEventRecord(c.evGE, c.cs));
+  TP_CUDA(cudaStreamWaitEvent(c.gs, c.evGE, 0));
+  reduce_and_update(E, c.gaccE);
+  // ---- a10: loss
+  if (c.world > 1) TP_NCCL(ncclAllReduce(c.d_loss, c.d_loss, 1, ncclFloat64, ncclSum, c.world_comm, c.cs));
+  TP_CUDA(cudaMemcpyAsync(c.h_loss, c.d_loss, sizeof(double), cudaMemcpyDeviceToHost, c.cs));
+  TP_CUDA(cudaEventRecord(c.ev_ws1, c.ws));
+  TP_CUDA(cudaEventRecord(c.ev_gs1, c.gs));
+  TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_ws1, 0));
+  TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_gs1, 0));
+  TP_CUDA(cudaEventRecord(c.ev_s1, c.cs));
+  TP_CUDA(cudaStreamSynchronize(c.cs));
+  TP_CUDA(cudaDeviceSynchronize());
+  // ---- stats
+  std::memset(c.stats, 0, sizeof(c.stats));
+  float ms = 0.f;
+  TP_CUDA(cudaEventElapsedTime(&ms, c.ev_s0, c.ev_s1));
+  c.stats[0] = ms;
+  if (c.timing) {
+    for (auto& r : c.regions) {
+      float e = 0.f;
+      TP_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+      switch (r.kind) {
+        case 0: c.stats[4] += e; c.stats[5] += r.work * 1e-9; c.stats[6] += 1; break;
+        case 1: c.stats[7] += e; c.stats[8] += r.work * 1e-9; break;
+        case 2: c.stats[9] += e; c.stats[10] += r.work * 1e-9; break;
+        case 3: c.stats[1] += e; break;
+        case 4: c.stats[14] += e; break;
+        case 5: break;
+      }
+    }
+    float wms = 0.f, gms = 0.f;
+    TP_CUDA(cudaEventElapsedTime(&wms, c.ev_ws0, c.ev_ws1));
+    TP_CUDA(cudaEventElapsedTime(&gms, c.ev_gs0, c.ev_gs1));
+    c.stats[2] = wms;
+    c.stats[3] = gms;
+  }
+  c.stats[11] = static_cast<double>(g_kstats.launches - c.launches_at_start);
+  c.stats[12] = static_cast<double>(c.bytes_alloc) * 1e-9;
+  c.stats[13] = static_cast<double>(c.esz);
+  return *c.h_loss / (static_cast<double>(c.N) * c.Bm * c.S);
+}
+
+// ------------------------------------------------------------------------------------ init
+int64_t pad_to(int64_t n, int G) {
+  const int64_t q = static_cast<int64_t>(G) * 64;
+  return q * ((n + q - 1) / q);
+}
+
+void build(int P, int G, int L, const tawpipe_dims* d, int N) {
+  Ctx& c = *g;
+  TP_CHECK(d != nullptr, TAWPIPE_ECONFIG, "dims is NULL");
+  TP_CHECK(P == c.world, TAWPIPE_ECONFIG, "n_devices (" + std::to_string(P) + ") != world size (" +
+                                              std::to_string(c.world) + ")");
+  TP_CHECK(G >= 1 && P % G == 0, TAWPIPE_ECONFIG, "P mod G != 0 (PAPER.md:53 requires P mod D = 0)");
+  const int D = P / G;
+  TP_CHECK(L >= 1 && L % D == 0, TAWPIPE_ECONFIG, "L mod D != 0 (striped DBS, reading R6)");
+  TP_CHECK(N >= 1 && N % P == 0, TAWPIPE_ECONFIG, "N mod P != 0 (even micro-batch split, R4)");
+  TP_CHECK(D <= 8, TAWPIPE_ECONFIG, "at most 8 groups");
+  TP_CHECK(d->hidden > 0 && d->heads > 0 && d->hidden % d->heads == 0, TAWPIPE_ECONFIG, "H mod n_h != 0");
+  TP_CHECK(d->ffn > 0 && d->vocab > 0 && d->seq > 0 && d->micro_bs > 0, TAWPIPE_ECONFIG, "non-positive dimension");
+  TP_CHECK((d->hidden / d->heads) % 2 == 0, TAWPIPE_ECONFIG, "d_h must be even (rotate-half RoPE)");
+  TP_CHECK(d->dtype == TAWPIPE_FP32 || d->dtype == TAWPIPE_BF16, TAWPIPE_ECONFIG, "dtype must be FP32 or BF16");
+  TP_CHECK(d->reserved == 0, TAWPIPE_ECONFIG, "reserved must be 0");
+  if (d->dtype == TAWPIPE_BF16) {
+    const int dh = d->hidden / d->heads;
+    TP_CHECK(dh == 64 || dh == 128, TAWPIPE_ECONFIG, "bf16 path: d_h must be 64 or 128");
+    TP_CHECK(d->seq % 128 == 0, TAWPIPE_ECONFIG, "bf16 path: S mod 128 != 0");
+    TP_CHECK(d->hidden % 128 == 0 && d->ffn % 128 == 0 && d->vocab % 128 == 0, TAWPIPE_ECONFIG,
+             "bf16 path: H, I, V must be multiples of 128");
+  }
+  c.P = P;
+  c.G = G;
+  c.D = D;
+  c.k = c.rank / G;
+  c.j = c.rank % G;
+  c.L = L;
+  c.N = N;
+  c.m = N / P;
+  c.dims = *d;
+  c.H = d->hidden;
+  c.nh = d->heads;
+  c.dh = d->hidden / d->heads;
+  c.I = d->ffn;
+  c.V = d->vocab;
+  c.S = d->seq;
+  c.Bm = d->micro_bs;
+  c.T = static_cast<int64_t>(c.Bm) * c.S;
+  c.bf = d->dtype == TAWPIPE_BF16;
+  c.esz = c.bf ? 2 : 4;
+  const int64_t H = c.H, I = c.I, V = c.V;
+  c.phi = 4 * H * H + 3 * H * I + 2 * H;
+  // ---- DBS plan (a1): units, ownership, stripes, canonical offsets, owned-state offsets
+  c.units.assign(L + 2, Unit{});
+  for (int l = 0; l < L + 2; ++l) {
+    Unit& u = c.units[l];
+    if (l < L) {
+      u.cls = U_BLOCK;
+      u.n = c.phi;
+      u.owner = l % D;
+      u.canon = V * H + static_cast<int64_t>(l) * c.phi;
+      u.n_nd = 2;  // RMSNorm gains: no weight decay (R1)
+      u.nd_lo[0] = 0;
+      u.nd_hi[0] = H;
+      u.nd_lo[1] = H + 4 * H * H;
+      u.nd_hi[1] = 2 * H + 4 * H * H;
+    } else if (l == L) {
+      u.cls = U_E;
+      u.n = V * H;
+      u.owner = 0;
+      u.canon = 0;
+    } else {
+      u.cls = U_F;
+      u.n = H + V * H;
+      u.owner = D - 1;
+      u.canon = V * H + static_cast<int64_t>(L) * c.phi;
+      u.n_nd = 1;
+      u.nd_lo[0] = 0;
+      u.nd_hi[0] = H;
+    }
+    u.n_pad = pad_to(u.n, G);
+    u.s = u.n_pad / G;
+    u.owned = (u.owner == c.k);
+    c.max_pad = std::max(c.max_pad, u.n_pad);
+    c.max_s = std::max(c.max_s, u.s);
+  }
+  c.owned_total = 0;
+  for (int l = 0; l < L + 2; ++l)  // canonical shard order: layers ascending, then E, then F
+    if (c.units[l].owned) {
+      c.units[l].off = c.owned_total;
+      c.owned_total += c.units[l].s;
+    }
+  // ---- streams, events, communicators
+  TP_CUDA(cudaStreamCreateWithFlags(&c.cs, cudaStreamNonBlocking));
+  TP_CUDA(cudaStreamCreateWithFlags(&c.ws, cudaStreamNonBlocking));
+  TP_CUDA(cudaStreamCreateWithFlags(&c.gs, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    TP_CUDA(cudaEventCreateWithFlags(&c.w_ready[i], cudaEventDisableTiming));
+    TP_CUDA(cudaEventCreateWithFlags(&c.w_free[i], cudaEventDisableTiming));
+    TP_CUDA(cudaEventCreateWithFlags(&c.g_ready[i], cudaEventDisableTiming));
+    TP_CUDA(cudaEventCreateWithFlags(&c.g_free[i], cudaEventDisableTiming));
+  }
+  for (cudaEvent_t* e : {&c.evE, &c.evF, &c.evGF, &c.evGE}) TP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&c.ev_s0, &c.ev_s1, &c.ev_ws0, &c.ev_ws1, &c.ev_gs0, &c.ev_gs1}) TP_CUDA(cudaEventCreate(e));
+  if (c.world > 1) {
+    // group communicator: color k, rank j ; rail communicator: color j, rank k (R5)
+    TP_NCCL(ncclCommSplit(c.world_comm, c.k, c.j, &c.wg, nullptr));
+    TP_NCCL(ncclCommSplit(c.world_comm, c.j, c.k, &c.wr, nullptr));
+    TP_NCCL(ncclCommSplit(c.world_comm, c.k, c.j, &c.gg, nullptr));
+    TP_NCCL(ncclCommSplit(c.world_comm, c.j, c.k, &c.gr, nullptr));
+  }
+  // ---- DBS state
+  const size_t esz = c.esz;
+  c.master = (float*)dmalloc(c.owned_total * 4);
+  c.mom = (float*)dmalloc(c.owned_total * 4);
+  c.vel = (float*)dmalloc(c.owned_total * 4);
+  c.wire = dmalloc(c.owned_total * esz);
+  TP_CUDA(cudaMemsetAsync(c.mom, 0, c.owned_total * 4, c.cs));
+  TP_CUDA(cudaMemsetAsync(c.vel, 0, c.owned_total * 4, c.cs));
+  const bool alias_layers = (G == 1 && D == 1);
+  if (!alias_layers) {
+    c.wbuf[0] = dmalloc(c.units[0].n_pad * esz);
+    c.wbuf[1] = dmalloc(c.units[0].n_pad * esz);
+  }
+  if (!(G == 1 && c.units[L].owned)) c.ebuf = dmalloc(c.units[L].n_pad * esz);
+  if (!(G == 1 && c.units[L + 1].owned)) c.fbuf = dmalloc(c.units[L + 1].n_pad * esz);
+  c.gacc[0] = (float*)dmalloc(c.units[0].n_pad * 4);
+  c.gacc[1] = (float*)dmalloc(c.units[0].n_pad * 4);
+  c.gaccE = (float*)dmalloc(c.units[L].n_pad * 4);
+  c.gaccF = (float*)dmalloc(c.units[L + 1].n_pad * 4);
+  TP_CUDA(cudaMemsetAsync(c.gacc[0], 0, c.units[0].n_pad * 4, c.cs));
+  TP_CUDA(cudaMemsetAsync(c.gacc[1], 0, c.units[0].n_pad * 4, c.cs));
+  if (G > 1 || D > 1) c.gwire = dmalloc(c.max_pad * esz);
+  if (G > 1) c.rsout = dmalloc(c.max_s * esz);
+  if (D > 1) c.crecv = dmalloc(c.max_s * (D - 1) * esz);
+  // ---- activations
+  const int64_t T = c.T;
+  const int m = c.m;
+  c.ck.resize(static_cast<size_t>(L + 1) * m);
+  for (auto& p : c.ck) p = dmalloc(T * H * esz);
+  const size_t n_acts = d->ckpt ? 1 : static_cast<size_t>(L) * m;
+  c.acts.resize(n_acts);
+  for (auto& A : c.acts) {
+    A.a = dmalloc(T * H * esz);
+    A.qkv = dmalloc(T * 3 * H * esz);
+    A.o = dmalloc(T * H * esz);
+    A.h1 = dmalloc(T * H * esz);
+    A.b = dmalloc(T * H * esz);
+    A.gu = dmalloc(T * 2 * I * esz);
+    A.y = dmalloc(T * I * esz);
+    A.r1 = (float*)dmalloc(T * 4);
+    A.r2 = (float*)dmalloc(T * 4);
+    A.lse = (float*)dmalloc(T * c.nh * 4);
+  }
+  c.dhb.resize(m);
+  for (auto& p : c.dhb) p = dmalloc(T * H * esz);
+  c.dY = dmalloc(T * I * esz);
+  c.dGU = dmalloc(T * 2 * I * esz);
+  c.db = dmalloc(T * H * esz);
+  c.dh1 = dmalloc(T * H * esz);
+  c.dO = dmalloc(T * H * esz);
+  c.dqkv = dmalloc(T * 3 * H * esz);
+  c.da = dmalloc(T * H * esz);
+  c.delta = (float*)dmalloc(T * c.nh * 4);
+  c.dq_acc = c.bf ? (float*)dmalloc(T * H * 4) : nullptr;
+  c.Tc = std::min<int64_t>(T, 8192);
+  c.fnorm = dmalloc(T * H * esz);
+  c.df = dmalloc(T * H * esz);
+  c.logits = dmalloc(c.Tc * V * esz);
+  c.rstd_f = (float*)dmalloc(T * 4);
+  c.loss_rows = (float*)dmalloc(T * 4);
+  c.d_loss = (double*)dmalloc(sizeof(double));
+  TP_CUDA(cudaMallocHost(&c.h_loss, sizeof(double)));
+  const int64_t tok_elems = static_cast<int64_t>(m) * c.Bm * (c.S + 1);
+  c.d_tok = (int32_t*)dmalloc(tok_elems * 4);
+  c.d_in = (int32_t*)dmalloc(static_cast<int64_t>(m) * T * 4);
+  c.d_tgt = (int32_t*)dmalloc(static_cast<int64_t>(m) * T * 4);
+  TP_CUDA(cudaMallocHost(&c.h_tok, tok_elems * 4));
+  // RoPE tables in fp64 on the host, stored fp32 (R13)
+  {
+    const int half = c.dh / 2;
+    std::vector<float> cs(static_cast<size_t>(c.S) * half), sn(cs.size());
+    for (int p = 0; p < c.S; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(static_cast<double>(d->rope_theta), -2.0 * i / c.dh);
+        const double ang = static_cast<double>(p) * inv;
+        cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(ang));
+        sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(ang));
+      }
+    c.cosT = (float*)dmalloc(cs.size() * 4);
+    c.sinT = (float*)dmalloc(sn.size() * 4);
+    TP_CUDA(cudaMemcpyAsync(c.cosT, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c.cs));
+    TP_CUDA(cudaMemcpyAsync(c.sinT, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c.cs));
+    TP_CUDA(cudaStreamSynchronize(c.cs));
+  }
+  // ---- seeded device-side initialisation of the owned stripes (R20)
+  for (int l = 0; l < L + 2; ++l) {
+    const Unit& u = c.units[l];
+    if (!u.owned) continue;
+    const int64_t lo = static_cast<int64_t>(c.j) * u.s;  // stripe start in unit coordinates
+    float* ms = c.master + u.off;
+    BY_TYPE(init_normal<float>((float*)wptr(c.wire, u.off), ms, u.s, u.canon + lo, d->seed, 0.02f, c.cs),
+            init_normal<bf16>((bf16*)wptr(c.wire, u.off), ms, u.s, u.canon + lo, d->seed, 0.02f, c.cs));
+    for (int r = 0; r < u.n_nd; ++r) {  // gains = 1
+      const int64_t a = std::max(u.nd_lo[r], lo), b = std::min(u.nd_hi[r], lo + u.s);
+      if (a < b) fill_f32(ms + (a - lo), b - a, 1.0f, c.cs);
+    }
+    if (u.n < lo + u.s) {  // zero padding
+      const int64_t a = std::max(u.n, lo);
+      fill_f32(ms + (a - lo), lo + u.s - a, 0.0f, c.cs);
+    }
+    BY_TYPE(cast_f32<float>(ms, (float*)wptr(c.wire, u.off), u.s, c.cs),
+            cast_f32<bf16>(ms, (bf16*)wptr(c.wire, u.off), u.s, c.cs));
+  }
+  TP_CUDA(cudaStreamSynchronize(c.cs));
+  c.inited = true;
+}
+
+void load(const float* full, int64_t n) {
+  Ctx& c = *g;
+  const int64_t expect = 2 * static_cast<int64_t>(c.V) * c.H + static_cast<int64_t>(c.L) * c.phi + c.H;
+  TP_CHECK(n == expect, TAWPIPE_ECONFIG, "tawpipe_load: expected " + std::to_string(expect) + " elements, got " +
+                                             std::to_string(n));
+  for (int l = 0; l < c.L + 2; ++l) {
+    const Unit& u = c.units[l];
+    if (!u.owned) continue;
+    const int64_t lo = static_cast<int64_t>(c.j) * u.s;
+    float* ms = c.master + u.off;
+    // every copy is ordered on c.cs: the compute stream is non-blocking and would not see legacy-stream copies
+    TP_CUDA(cudaMemsetAsync(ms, 0, u.s * 4, c.cs));
+    const int64_t valid = std::max<int64_t>(0, std::min(u.n, lo + u.s) - lo);
+    if (valid > 0) TP_CUDA(cudaMemcpyAsync(ms, full + u.canon + lo, valid * 4, cudaMemcpyHostToDevice, c.cs));
+    BY_TYPE(cast_f32<float>(ms, (float*)wptr(c.wire, u.off), u.s, c.cs),
+            cast_f32<bf16>(ms, (bf16*)wptr(c.wire, u.off), u.s, c.cs));
+  }
+  TP_CUDA(cudaMemsetAsync(c.mom, 0, c.owned_total * 4, c.cs));
+  TP_CUDA(cudaMemsetAsync(c.vel, 0, c.owned_total * 4, c.cs));
+  TP_CUDA(cudaStreamSynchronize(c.cs));
+  c.step_t = 0;
+}
+
+void destroy() {
+  if (!g) return;
+  cudaDeviceSynchronize();
+  for (void* p : g->allocs) cudaFree(p);
+  if (g->h_tok) cudaFreeHost(g->h_tok);
+  if (g->h_loss) cudaFreeHost(g->h_loss);
+  for (ncclComm_t cm : {g->wg, g->wr, g->gg, g->gr})
+    if (cm) ncclCommDestroy(cm);
+  if (g->world_comm) ncclCommDestroy(g->world_comm);
+  for (cudaEvent_t e : g->ev_pool) cudaEventDestroy(e);
+  if (g->cs) cudaStreamDestroy(g->cs);
+  if (g->ws) cudaStreamDestroy(g->ws);
+  if (g->gs) cudaStreamDestroy(g->gs);
+  delete g;
+  g = nullptr;
+}
+
+template <typename F>
+int guarded(F f) {
+  try {
+    f();
+    return TAWPIPE_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TAWPIPE_ERUNTIME;
+  }
+}
+
+}  // namespace
+}  // namespace tp
+
+using namespace tp;
+
+extern "C" {
+
+int tawpipe_get_unique_id(void* out) {
+  return guarded([&] {
+    TP_CHECK(out, TAWPIPE_ECONFIG, "out is NULL");
+    ncclUniqueId id;
+    TP_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int tawpipe_bootstrap(int rank, int world, int device, const void* uid) {
+  return guarded([&] {
+    TP_CHECK(world >= 1 && rank >= 0 && rank < world, TAWPIPE_ECONFIG, "bad rank/world");
+    if (g) destroy();
+    g = new Ctx();
+    g->rank = rank;
+    g->world = world;
+    g->device = device;
+    TP_CUDA(cudaSetDevice(device));
+    if (world > 1) {
+      TP_CHECK(uid, TAWPIPE_ECONFIG, "unique_id required when world > 1");
+      ncclUniqueId id;
+      std::memcpy(&id, uid, sizeof(id));
+      TP_NCCL(ncclCommInitRank(&g->world_comm, world, id, rank));
+    }
+    g->booted = true;
+  });
+}
+
+int tawpipe_init(int n_devices, int group_size, int n_layers, const tawpipe_dims* dims, int n_micro) {
+  if (!g || !g->booted) {
+    g_err = "tawpipe_init before tawpipe_bootstrap";
+    return TAWPIPE_EUNINIT;
+  }
+  if (g->inited) {
+    g_err = "already initialised; call tawpipe_finalize first";
+    return TAWPIPE_ECONFIG;
+  }
+  return guarded([&] { build(n_devices, group_size, n_layers, dims, n_micro); });
+}
+
+int tawpipe_load(const float* full, int64_t n) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  return guarded([&] {
+    TP_CHECK(full, TAWPIPE_ECONFIG, "full_model is NULL");
+    load(full, n);
+  });
+}
+
+static float step_common(const int32_t* tok, bool dev) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return NAN;
+  }
+  double loss = NAN;
+  int rc = guarded([&] {
+    TP_CHECK(tok, TAWPIPE_ECONFIG, "tokens is NULL");
+    loss = run_step(tok, dev);
+  });
+  return rc == TAWPIPE_OK ? static_cast<float>(loss) : NAN;
+}
+
+float tawpipe_step(const int32_t* tokens) { return step_common(tokens, false); }
+float tawpipe_step_device(const int32_t* dev_tokens) { return step_common(dev_tokens, true); }
+
+int64_t tawpipe_shard_elems(void) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  return g->owned_total;
+}
+
+int64_t tawpipe_shard(float* out) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  int rc = guarded([&] {
+    TP_CHECK(out, TAWPIPE_ECONFIG, "out is NULL");
+    TP_CUDA(cudaDeviceSynchronize());
+    TP_CUDA(cudaMemcpy(out, g->master, g->owned_total * 4, cudaMemcpyDeviceToHost));
+  });
+  return rc == TAWPIPE_OK ? g->owned_total : rc;
+}
+
+int tawpipe_ledger(uint64_t* out, int n) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  if (!out || n < TAWPIPE_LEDGER_N) {
+    g_err = "ledger buffer too small";
+    return TAWPIPE_ECONFIG;
+  }
+  std::memcpy(out, g->ledger, sizeof(g->ledger));
+  return TAWPIPE_OK;
+}
+
+int tawpipe_stats(double* out, int n) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  if (!out || n < TAWPIPE_STATS_N) {
+    g_err = "stats buffer too small";
+    return TAWPIPE_ECONFIG;
+  }
+  std::memcpy(out, g->stats, sizeof(g->stats));
+  return TAWPIPE_OK;
+}
+
+int tawpipe_set_timing(int on) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  g->timing = on != 0;
+  return TAWPIPE_OK;
+}
+
+const char* tawpipe_last_error(void) { return g_err.c_str(); }
+
+void tawpipe_finalize(void) { destroy(); }
+
+int tawpipe_gemm(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t a_ld, int a_kmajor, const void* B,
+                 int64_t b_ld, int b_kmajor, void* C, int64_t c_ld, int c_f32, int accumulate, const void* R,
+                 void* stream) {
+  return guarded([&] {
+    GemmArgs a{M, N, K, A, a_ld, a_kmajor != 0, B, b_ld, b_kmajor != 0, C, c_ld, c_f32 != 0, accumulate != 0, R};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dtype == TAWPIPE_BF16) {
+      const char* e = std::getenv("TAWPIPE_GEMM");
+      if (e && std::string(e) == "simt")
+        gemm_simt<bf16>(a, s);
+      else
+        gemm_tc_bf16(a, s);
+    } else if (dtype == TAWPIPE_FP32) {
+      gemm_simt<float>(a, s);
+    } else {
+      throw Error(TAWPIPE_ECONFIG, "bad dtype");
+    }
+  });
+}
+
+int tawpipe_attention_fwd(int dtype, int B, int S, int n_h, int d_h, const void* qkv, void* o, float* lse,
+                          void* stream) {
+  return guarded([&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dtype == TAWPIPE_FP32)
+      attention_fwd_simt<float>(B, S, n_h, d_h, (const float*)qkv, (float*)o, lse, s);
+    else if (attention_tc_supported(S, d_h) && !(std::getenv("TAWPIPE_ATTN") && std::string(std::getenv("TAWPIPE_ATTN")) == "simt"))
+      attention_fwd_tc(B, S, n_h, d_h, (const bf16*)qkv, (bf16*)o, lse, s);
+    else
+      attention_fwd_simt<bf16>(B, S, n_h, d_h, (const bf16*)qkv, (bf16*)o, lse, s);
+  });
+}
+
+int tawpipe_attention_bwd(int dtype, int B, int S, int n_h, int d_h, const void* qkv, const void* o, const float* lse,
+                          const void* do_, void* dqkv, float* delta, float* dq_acc, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dtype == TAWPIPE_FP32)
+      attention_bwd_simt<float>(B, S, n_h, d_h, (const float*)qkv, (const float*)o, lse, (const float*)do_,
+                                (float*)dqkv, delta, s);
+    else if (attention_tc_supported(S, d_h) && !(std::getenv("TAWPIPE_ATTN") && std::string(std::getenv("TAWPIPE_ATTN")) == "simt"))
+      attention_bwd_tc(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv, delta,
+                       dq_acc, s);
+    else
+      attention_bwd_simt<bf16>(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv,
+                               delta, s);
+  });
+}
+
+}  // extern "C"

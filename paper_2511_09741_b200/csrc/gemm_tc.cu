@@ -1,0 +1,325 @@
+// gemm_tc.cu -- persistent, warp-specialised tcgen05 GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM).
+//
+//   C[M,N] (+)= Σ_k A(m,k) · B(n,k)      (+ R[M,N] residual)
+//
+// Used for every dense contraction of the decoder layer (QKV, O, gate/up, down,
+// their dgrad and wgrad, and the LM head), which are the method's "dense contractions" (north_star).
+//   forward  y  = x·Wᵀ   : A = x  (K-major), B = W  (K-major)
+//   dgrad    dx = dy·W   : A = dy (K-major), B = W  (MN-major: contraction runs over W's rows)
+//   wgrad    dW += dyᵀ·x : A = dy (MN-major), B = x (MN-major), C fp32 accumulate (grad accumulator)
+//
+// Roles (192 threads, one CTA per SM, persistent over output tiles):
+//   warp 0  TMA producer: 128×64 A tile + BN×64 B tile per stage, SWIZZLE_128B, mbarrier complete_tx
+//   warp 1  MMA issuer:   one thread issues 4 × tcgen05.mma (M=128, N=BN, K=16) per stage into a TMEM
+//                         accumulator; tcgen05.commit frees the smem stage / publishes the accumulator
+//   warps 2-5 epilogue:   tcgen05.ld 32 columns at a time → fp32 → (+R / +=C) → bf16 or fp32 stores
+// Two TMEM accumulators (2 × BN columns) let the epilogue of tile i overlap the mainloop of tile i+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace tp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;   // 32 / 16 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+enum Epi : int { EPI_BF16 = 0, EPI_F32_STORE = 1, EPI_F32_ACC = 2 };
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
+                   int64_t ldc, const bf16* __restrict__ R, int M, int N, int K) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + Cfg::STAGES;
+  uint64_t* tfull = bars + 2 * Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int num_m = M / BM, num_n = N / BN, num_k = K / BK;
+  const int num_tiles = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < Cfg::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // grouped rasterisation: 16 M-tiles share each sweep over N for L2 reuse
+  auto tile_coords = [&](int t, int& mb, int& nb) {
+    constexpr int GROUP = 16;
+    const int group_size = GROUP * num_n;
+    const int g = t / group_size;
+    const int first_m = g * GROUP;
+    const int gm = min(GROUP, num_m - first_m);
+    const int r = t % group_size;
+    mb = first_m + r % gm;
+    nb = r / gm;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, mb, nb);
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (!A_MN) {
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i) tma_load_2d(sa + i * 8192, &tmA, &full[stage], mb * BM + i * 64, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) tma_load_2d(sb + i * 8192, &tmB, &full[stage], nb * BN + i * 64, kb * BK);
+          }
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(sa + k * 2048, 8192, 1024) : umma_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(sb + k * 2048, 8192, 1024) : umma_desc_sw128(sb + k * 32, 16, 1024);
+            umma_f16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(mb) * BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c, r);
+        tmem_wait_ld();
+        const int64_t col = static_cast<int64_t>(nb) * BN + c;
+        if (EPI == EPI_BF16) {
+          bf16* dst = reinterpret_cast<bf16*>(C) + row * ldc + col;
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+          if (R != nullptr) {
+            const uint4* rs = reinterpret_cast<const uint4*>(R + row * ldc + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 x = rs[v];
+              const bf16* xb = reinterpret_cast<const bf16*>(&x);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[v * 8 + i] += __bfloat162float(xb[i]);
+            }
+          }
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 o;
+            o.x = pack_bf16(f[v * 8 + 0], f[v * 8 + 1]);
+            o.y = pack_bf16(f[v * 8 + 2], f[v * 8 + 3]);
+            o.z = pack_bf16(f[v * 8 + 4], f[v * 8 + 5]);
+            o.w = pack_bf16(f[v * 8 + 6], f[v * 8 + 7]);
+            d4[v] = o;
+          }
+        } else {
+          float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + row * ldc + col);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            if (EPI == EPI_F32_ACC) {
+              const float4 p = d4[v];
+              o.x += p.x;
+              o.y += p.y;
+              o.z += p.z;
+              o.w += p.w;
+            }
+            d4[v] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    TP_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q));
+    TP_CHECK(q == cudaDriverEntryPointSuccess && p, TAWPIPE_ERUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+// 2-D bf16 tensor map: inner dimension `inner` (contiguous), outer dimension `outer` with row pitch `ld`
+// elements; box = 64 inner × box_outer, 128-byte swizzle.
+CUtensorMap make_tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TP_CHECK(r == CUDA_SUCCESS, TAWPIPE_ERUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return m;
+}
+
+namespace {
+
+int g_num_sms = 0;
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void launch(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr_set = true;
+  }
+  if (g_num_sms == 0) {
+    int dev;
+    TP_CUDA(cudaGetDevice(&dev));
+    TP_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  // A: K-major -> rows M, inner K ; MN-major -> inner M, rows K
+  CUtensorMap ta = A_MN ? make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, 64) : make_tmap_bf16_2d(g.A, g.K, g.M, g.lda, BM);
+  CUtensorMap tb = B_MN ? make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 64) : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, BN);
+  const int tiles = static_cast<int>((g.M / BM) * (g.N / BN));
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
+                                     static_cast<int>(g.N), static_cast<int>(g.K));
+  TP_CUDA(cudaGetLastError());
+  g_kstats.launches++;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
+  if (!g.c_f32)
+    launch<BN, A_MN, B_MN, EPI_BF16>(g, s);
+  else if (g.accumulate)
+    launch<BN, A_MN, B_MN, EPI_F32_ACC>(g, s);
+  else
+    launch<BN, A_MN, B_MN, EPI_F32_STORE>(g, s);
+}
+
+template <int BN>
+void dispatch_major(const GemmArgs& g, cudaStream_t s) {
+  const bool a_mn = !g.a_kmajor, b_mn = !g.b_kmajor;
+  if (!a_mn && !b_mn) dispatch_epi<BN, false, false>(g, s);
+  else if (!a_mn && b_mn) dispatch_epi<BN, false, true>(g, s);
+  else if (a_mn && b_mn) dispatch_epi<BN, true, true>(g, s);
+  else dispatch_epi<BN, true, false>(g, s);
+}
+
+}  // namespace
+
+void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
+  TP_CHECK(g.M % BM == 0 && g.K % BK == 0 && g.N % 128 == 0, TAWPIPE_ECONFIG,
+           "tcgen05 GEMM needs M%128==0, N%128==0, K%64==0 (got " + std::to_string(g.M) + "x" +
+               std::to_string(g.N) + "x" + std::to_string(g.K) + ")");
+  TP_CHECK(!(g.accumulate && !g.c_f32), TAWPIPE_ECONFIG, "bf16 accumulate-into-C is not supported; use R");
+  TP_CHECK(!(g.R && g.c_f32), TAWPIPE_ECONFIG, "residual only with bf16 C");
+  TP_CHECK((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B) | reinterpret_cast<uintptr_t>(g.C)) %
+                   16 == 0 &&
+               g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0,
+           TAWPIPE_ECONFIG, "tcgen05 GEMM needs 16-byte aligned operands and leading dimensions");
+  if (g.N % 256 == 0)
+    dispatch_major<256>(g, s);
+  else
+    dispatch_major<128>(g, s);
+}
+
+}  // namespace tp

@@ -1,0 +1,413 @@
+// kernels.cu -- HBM-bound kernels of the step: embedding, RMSNorm, RoPE, SwiGLU, cross-entropy, casts,
+// initialisation and the fused gradient-accumulate + AdamW update on the owned DBS stripe.
+// Formulas: SURVEY.md §8(c) (forward algorithm and backward-formula table); AdamW: PyTorch semantics (R1).
+// All reductions run in fp32 regardless of the storage type T (float or bf16).
+#include "common.cuh"
+
+namespace tp {
+
+KernelStats g_kstats;
+
+namespace {
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) t += red[i];
+  return t;
+}
+
+template <int NT>
+__device__ __forceinline__ float block_max(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NT / 32; ++i) t = fmaxf(t, red[i]);
+  return t;
+}
+
+inline unsigned blocks_for(int64_t n, int per_block) {
+  int64_t b = (n + per_block - 1) / per_block;
+  return static_cast<unsigned>(b < 1 ? 1 : (b > (1ll << 30) ? (1ll << 30) : b));
+}
+
+#define LAUNCHED() \
+  do {             \
+    TP_CUDA(cudaGetLastError()); \
+    g_kstats.launches++;         \
+  } while (0)
+
+// ------------------------------------------------------------------------------------ embedding (a4)
+template <typename T>
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, int64_t stride_seq, int S, const T* __restrict__ E,
+                                 int H, T* __restrict__ h) {
+  const int64_t row = blockIdx.x;  // b*S + p
+  const int b = static_cast<int>(row / S), p = static_cast<int>(row % S);
+  const int64_t t = tok[b * stride_seq + p];
+  for (int c = threadIdx.x; c < H; c += blockDim.x) h[row * H + c] = E[t * H + c];
+}
+
+template <typename T>
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, int64_t stride_seq, int S, const T* __restrict__ dh,
+                                 int H, float* __restrict__ dE) {
+  const int64_t row = blockIdx.x;
+  const int b = static_cast<int>(row / S), p = static_cast<int>(row % S);
+  const int64_t t = tok[b * stride_seq + p];
+  for (int c = threadIdx.x; c < H; c += blockDim.x) atomicAdd(&dE[t * H + c], to_f(dh[row * H + c]));
+}
+
+// ------------------------------------------------------------------------------------ RMSNorm
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) rmsnorm_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                         T* __restrict__ y, float* __restrict__ rstd, int H,
+                                                         float eps) {
+  __shared__ float red[NT / 32];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * H;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < H; c += NT) {
+    const float v = to_f(xr[c]);
+    ss += v * v;
+  }
+  ss = block_sum<NT>(ss, red);
+  const float r = rsqrtf(ss / H + eps);
+  if (threadIdx.x == 0) rstd[row] = r;
+  for (int c = threadIdx.x; c < H; c += NT) y[row * H + c] = from_f<T>(to_f(xr[c]) * r * to_f(g[c]));
+}
+
+// dγ = Σ_rows dy⊙x·r ; with gg = dy⊙γ: dx = r·gg − x·r³·mean_H(gg⊙x)   (+ res)
+template <typename T, int NT, int RB>
+__global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                         const T* __restrict__ g, const float* __restrict__ rstd,
+                                                         const T* __restrict__ res, T* __restrict__ dx,
+                                                         float* __restrict__ dg_acc, int64_t rows, int H) {
+  extern __shared__ float dg_part[];  // [H]
+  __shared__ float red[NT / 32];
+  for (int c = threadIdx.x; c < H; c += NT) dg_part[c] = 0.f;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * RB;
+  for (int64_t row = r0; row < r0 + RB && row < rows; ++row) {
+    const float r = rstd[row];
+    const T* dyr = dy + row * H;
+    const T* xr = x + row * H;
+    float dot = 0.f;
+    for (int c = threadIdx.x; c < H; c += NT) {
+      const float d = to_f(dyr[c]), xv = to_f(xr[c]);
+      dot += d * to_f(g[c]) * xv;
+      dg_part[c] += d * xv * r;
+    }
+    dot = block_sum<NT>(dot, red);
+    const float coef = r * r * r * dot / H;
+    for (int c = threadIdx.x; c < H; c += NT) {
+      const float d = to_f(dyr[c]), xv = to_f(xr[c]);
+      float v = r * d * to_f(g[c]) - xv * coef;
+      if (res) v += to_f(res[row * H + c]);
+      dx[row * H + c] = from_f<T>(v);
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += NT) atomicAdd(&dg_acc[c], dg_part[c]);
+}
+
+// ------------------------------------------------------------------------------------ RoPE (rotate-half)
+// qkv rows of width ncols_blocks·H? No: rows are [q | k | v] of width 3H; blocks 0 (q) and 1 (k) are rotated.
+template <typename T>
+__global__ void rope_kernel(T* __restrict__ qkv, int64_t rows, int S, int nh, int dh, int64_t ld,
+                            const float* __restrict__ cs, const float* __restrict__ sn, int inverse, int nblk) {
+  const int half = dh / 2;
+  const int64_t per_row = static_cast<int64_t>(nblk) * nh * half;
+  const int64_t total = rows * per_row;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = idx / per_row;
+    int rem = static_cast<int>(idx % per_row);
+    const int i = rem % half;
+    rem /= half;
+    const int h = rem % nh;
+    const int blk = rem / nh;
+    const int p = static_cast<int>(row % S);
+    const float c = cs[static_cast<int64_t>(p) * half + i];
+    const float s = inverse ? -sn[static_cast<int64_t>(p) * half + i] : sn[static_cast<int64_t>(p) * half + i];
+    T* base = qkv + row * ld + static_cast<int64_t>(blk) * nh * dh + static_cast<int64_t>(h) * dh;
+    const float x1 = to_f(base[i]), x2 = to_f(base[i + half]);
+    base[i] = from_f<T>(x1 * c - x2 * s);
+    base[i + half] = from_f<T>(x2 * c + x1 * s);
+  }
+}
+
+// ------------------------------------------------------------------------------------ SwiGLU
+__device__ __forceinline__ float sigmoidf_(float u) { return 1.f / (1.f + __expf(-u)); }
+
+template <typename T>
+__global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ y, int64_t rows, int I) {
+  const int64_t total = rows * I;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / I;
+    const int c = static_cast<int>(idx % I);
+    const float u = to_f(gu[r * 2 * I + c]), w = to_f(gu[r * 2 * I + I + c]);
+    y[idx] = from_f<T>(u * sigmoidf_(u) * w);
+  }
+}
+
+// du = dy⊙w⊙σ(u)(1 + u(1−σ(u))) ; dw = dy⊙SiLU(u)
+template <typename T>
+__global__ void swiglu_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ gu, T* __restrict__ dgu,
+                                  int64_t rows, int I) {
+  const int64_t total = rows * I;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / I;
+    const int c = static_cast<int>(idx % I);
+    const float u = to_f(gu[r * 2 * I + c]), w = to_f(gu[r * 2 * I + I + c]);
+    const float d = to_f(dy[idx]);
+    const float sg = sigmoidf_(u);
+    dgu[r * 2 * I + c] = from_f<T>(d * w * sg * (1.f + u * (1.f - sg)));
+    dgu[r * 2 * I + I + c] = from_f<T>(d * u * sg);
+  }
+}
+
+// ------------------------------------------------------------------------------------ cross-entropy (a6)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) ce_kernel(T* __restrict__ z, const int32_t* __restrict__ tgt, int V,
+                                                float inv_denom, float* __restrict__ loss_rows) {
+  __shared__ float red[NT / 32];
+  const int64_t row = blockIdx.x;
+  T* zr = z + row * V;
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += NT) mx = fmaxf(mx, to_f(zr[c]));
+  mx = block_max<NT>(mx, red);
+  float se = 0.f;
+  for (int c = threadIdx.x; c < V; c += NT) se += __expf(to_f(zr[c]) - mx);
+  se = block_sum<NT>(se, red);
+  const float lse = mx + __logf(se);
+  const int t = tgt[row];
+  const float zt = to_f(zr[t]);
+  __syncthreads();
+  if (threadIdx.x == 0) loss_rows[row] = lse - zt;
+  for (int c = threadIdx.x; c < V; c += NT) {
+    float p = __expf(to_f(zr[c]) - lse);
+    if (c == t) p -= 1.f;
+    zr[c] = from_f<T>(p * inv_denom);
+  }
+}
+
+__global__ void sum_f64_kernel(const float* __restrict__ x, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < static_cast<int>(blockDim.x / 32); ++i) t += red[i];
+    *out += t;
+  }
+}
+
+// ------------------------------------------------------------------------------------ casts / init
+template <typename T>
+__global__ void cast_f32_kernel(const float* __restrict__ x, T* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = from_f<T>(x[i]);
+}
+template <typename T>
+__global__ void cast_to_f32_kernel(const T* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = to_f(x[i]);
+}
+__global__ void fill_kernel(float* __restrict__ x, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// counter-based N(0, std): Box-Muller on two uniforms derived from (seed, global index)
+template <typename T>
+__global__ void init_normal_kernel(T* __restrict__ wire, float* __restrict__ master, int64_t n, int64_t off,
+                                   uint64_t seed, float std) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h = splitmix64(seed ^ splitmix64(static_cast<uint64_t>(off + i)));
+    const float u1 = (static_cast<float>(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+    const float u2 = static_cast<float>((h >> 16) & 0xFFFFFFull) * (1.0f / 16777216.0f);
+    const float v = std * sqrtf(-2.f * __logf(u1)) * __cosf(6.2831853071795864f * u2);
+    master[i] = v;
+    wire[i] = from_f<T>(v);
+  }
+}
+
+// ------------------------------------------------------------------------------------ fused AdamW (a9)
+struct Contribs {
+  const void* p[8];
+};
+
+template <typename W>
+__global__ void adamw_kernel(Contribs c, int n_contrib, int own_k, int own_f32, float* __restrict__ master,
+                             float* __restrict__ m, float* __restrict__ v, W* __restrict__ wire, int64_t n,
+                             int64_t unit_off, int64_t nd0_lo, int64_t nd0_hi, int64_t nd1_lo, int64_t nd1_hi,
+                             AdamParams hp) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float g = 0.f;
+    for (int k = 0; k < n_contrib; ++k) {  // ascending group index (R16)
+      if (k == own_k && own_f32)
+        g += static_cast<const float*>(c.p[k])[i];
+      else
+        g += to_f(static_cast<const W*>(c.p[k])[i]);
+    }
+    const int64_t pos = unit_off + i;
+    const bool decay = !((pos >= nd0_lo && pos < nd0_hi) || (pos >= nd1_lo && pos < nd1_hi));
+    float th = master[i];
+    if (decay) th *= 1.f - hp.lr * hp.wd;
+    const float mi = hp.beta1 * m[i] + (1.f - hp.beta1) * g;
+    const float vi = hp.beta2 * v[i] + (1.f - hp.beta2) * g * g;
+    const float denom = sqrtf(vi / hp.bc2) + hp.eps;
+    th -= hp.lr * (mi / hp.bc1) / denom;
+    master[i] = th;
+    m[i] = mi;
+    v[i] = vi;
+    wire[i] = from_f<W>(th);
+  }
+}
+
+inline unsigned grid_stride_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+template <typename T>
+void embed_fwd(const int32_t* tok, int64_t stride_seq, int B, int S, const T* E, int H, T* h, cudaStream_t s) {
+  embed_fwd_kernel<T><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S, E, H, h);
+  LAUNCHED();
+}
+void embed_bwd(const int32_t* tok, int64_t stride_seq, int B, int S, const void* dh, bool dh_f32, int H, float* dE,
+               cudaStream_t s) {
+  if (dh_f32)
+    embed_bwd_kernel<float><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S,
+                                                                          static_cast<const float*>(dh), H, dE);
+  else
+    embed_bwd_kernel<bf16><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S,
+                                                                         static_cast<const bf16*>(dh), H, dE);
+  LAUNCHED();
+}
+template <typename T>
+void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
+  rmsnorm_fwd_kernel<T, 256><<<static_cast<unsigned>(rows), 256, 0, s>>>(x, g, y, rstd, H, eps);
+  LAUNCHED();
+}
+template <typename T>
+void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
+                 int64_t rows, int H, cudaStream_t s) {
+  constexpr int RB = 32;
+  const size_t smem = static_cast<size_t>(H) * sizeof(float);
+  if (smem > 48 * 1024) {
+    TP_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel<T, 256, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  }
+  rmsnorm_bwd_kernel<T, 256, RB><<<blocks_for(rows, RB), 256, smem, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H);
+  LAUNCHED();
+}
+template <typename T>
+void rope_apply(T* qkv, int B, int S, int nh, int dh, const float* cs, const float* sn, bool inverse, int nblk,
+                cudaStream_t s) {
+  const int64_t rows = static_cast<int64_t>(B) * S;
+  const int64_t total = rows * nblk * nh * (dh / 2);
+  rope_kernel<T><<<grid_stride_blocks(total), 256, 0, s>>>(qkv, rows, S, nh, dh, 3ll * nh * dh, cs, sn,
+                                                          inverse ? 1 : 0, nblk);
+  LAUNCHED();
+}
+template <typename T>
+void swiglu_fwd(const T* gu, T* y, int64_t rows, int I, cudaStream_t s) {
+  swiglu_fwd_kernel<T><<<grid_stride_blocks(rows * I), 256, 0, s>>>(gu, y, rows, I);
+  LAUNCHED();
+}
+template <typename T>
+void swiglu_bwd(const T* dy, const T* gu, T* dgu, int64_t rows, int I, cudaStream_t s) {
+  swiglu_bwd_kernel<T><<<grid_stride_blocks(rows * I), 256, 0, s>>>(dy, gu, dgu, rows, I);
+  LAUNCHED();
+}
+template <typename T>
+void cross_entropy(T* logits, const int32_t* targets, int64_t rows, int V, float inv_denom, float* loss_rows,
+                   cudaStream_t s) {
+  ce_kernel<T, 512><<<static_cast<unsigned>(rows), 512, 0, s>>>(logits, targets, V, inv_denom, loss_rows);
+  LAUNCHED();
+}
+void sum_f32_to_f64(const float* x, int64_t n, double* out, cudaStream_t s) {
+  sum_f64_kernel<<<1, 1024, 0, s>>>(x, n, out);
+  LAUNCHED();
+}
+template <typename T>
+void cast_f32(const float* x, T* y, int64_t n, cudaStream_t s) {
+  cast_f32_kernel<T><<<grid_stride_blocks(n), 256, 0, s>>>(x, y, n);
+  LAUNCHED();
+}
+template <typename T>
+void cast_to_f32(const T* x, float* y, int64_t n, cudaStream_t s) {
+  cast_to_f32_kernel<T><<<grid_stride_blocks(n), 256, 0, s>>>(x, y, n);
+  LAUNCHED();
+}
+void fill_f32(float* x, int64_t n, float v, cudaStream_t s) {
+  fill_kernel<<<grid_stride_blocks(n), 256, 0, s>>>(x, n, v);
+  LAUNCHED();
+}
+template <typename T>
+void init_normal(T* wire, float* master, int64_t n, int64_t global_off, uint64_t seed, float std, cudaStream_t s) {
+  init_normal_kernel<T><<<grid_stride_blocks(n), 256, 0, s>>>(wire, master, n, global_off, seed, std);
+  LAUNCHED();
+}
+template <typename W>
+void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_f32, float* master, float* m, float* v,
+                 W* wire, int64_t n, int64_t unit_off, const int64_t* nd_lo, const int64_t* nd_hi, int n_nd,
+                 AdamParams p, cudaStream_t s) {
+  TP_CHECK(n_contrib >= 1 && n_contrib <= 8, TAWPIPE_ECONFIG, "adamw: 1..8 group contributions supported");
+  Contribs c{};
+  for (int k = 0; k < n_contrib; ++k) c.p[k] = contrib[k];
+  const int64_t l0 = n_nd > 0 ? nd_lo[0] : 0, h0 = n_nd > 0 ? nd_hi[0] : 0;
+  const int64_t l1 = n_nd > 1 ? nd_lo[1] : 0, h1 = n_nd > 1 ? nd_hi[1] : 0;
+  adamw_kernel<W><<<grid_stride_blocks(n), 256, 0, s>>>(c, n_contrib, own_k, own_f32 ? 1 : 0, master, m, v, wire, n,
+                                                        unit_off, l0, h0, l1, h1, p);
+  LAUNCHED();
+}
+
+#define INST(T)                                                                                                    \
+  template void embed_fwd<T>(const int32_t*, int64_t, int, int, const T*, int, T*, cudaStream_t);                \
+  template void rmsnorm_fwd<T>(const T*, const T*, T*, float*, int64_t, int, float, cudaStream_t);              \
+  template void rmsnorm_bwd<T>(const T*, const T*, const T*, const float*, const T*, T*, float*, int64_t, int,   \
+                               cudaStream_t);                                                                    \
+  template void rope_apply<T>(T*, int, int, int, int, const float*, const float*, bool, int, cudaStream_t);     \
+  template void swiglu_fwd<T>(const T*, T*, int64_t, int, cudaStream_t);                                         \
+  template void swiglu_bwd<T>(const T*, const T*, T*, int64_t, int, cudaStream_t);                               \
+  template void cross_entropy<T>(T*, const int32_t*, int64_t, int, float, float*, cudaStream_t);                 \
+  template void cast_f32<T>(const float*, T*, int64_t, cudaStream_t);                                            \
+  template void cast_to_f32<T>(const T*, float*, int64_t, cudaStream_t);                                         \
+  template void init_normal<T>(T*, float*, int64_t, int64_t, uint64_t, float, cudaStream_t);                     \
+  template void adamw_fused<T>(const void* const*, int, int, bool, float*, float*, float*, T*, int64_t, int64_t, \
+                               const int64_t*, const int64_t*, int, AdamParams, cudaStream_t);
+INST(float)
+INST(bf16)
+
+}  // namespace tp

@@ -1,0 +1,151 @@
+"""Per-kernel parity on a B200 through the C ABI: tcgen05 GEMM (all operand majors and epilogues) against a
+plain PyTorch fp32 reference, and the attention kernels against the fp64 oracle's per-op functions."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from helpers import om  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2511_09741_b200 import tawpipe
+    tawpipe.lib()
+    return tawpipe
+
+
+def mk(shape, seed, dtype=torch.bfloat16):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randn(shape, generator=g) * 0.5).to(dtype).cuda()
+
+
+SHAPES = [(128, 128, 64), (256, 512, 320), (384, 384, 128), (512, 768, 1024), (1024, 256, 4096),
+          (4096, 4096, 256), (2048, 3200, 512)]   # last two: several tiles per persistent CTA
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, False), (False, True)])
+def test_tcgen05_gemm_majors_bf16_out(T, M, N, K, a_k, b_k):
+    A = mk((M, K) if a_k else (K, M), 1 + M)
+    B = mk((N, K) if b_k else (K, N), 2 + N)
+    C = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    T.gemm(T.BF16, M, N, K, A.data_ptr(), K if a_k else M, a_k, B.data_ptr(), K if b_k else N, b_k,
+           C.data_ptr(), N)
+    torch.cuda.synchronize()
+    Af = A.float() if a_k else A.float().t()
+    Bf = B.float() if b_k else B.float().t()
+    ref = Af @ Bf.t()
+    err = (C.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 320), (384, 384, 1024)])
+def test_tcgen05_gemm_f32_store_accumulate_residual(T, M, N, K):
+    A, B = mk((K, M), 3), mk((K, N), 4)          # wgrad form: both MN-major
+    ref = A.float().t() @ B.float()
+    C = torch.full((M, N), 0.25, dtype=torch.float32, device="cuda")
+    T.gemm(T.BF16, M, N, K, A.data_ptr(), M, False, B.data_ptr(), N, False, C.data_ptr(), N, c_f32=True,
+           accumulate=True)
+    torch.cuda.synchronize()
+    assert ((C - 0.25 - ref).abs().max() / ref.abs().max()).item() < 1e-5
+    T.gemm(T.BF16, M, N, K, A.data_ptr(), M, False, B.data_ptr(), N, False, C.data_ptr(), N, c_f32=True)
+    torch.cuda.synchronize()
+    assert ((C - ref).abs().max() / ref.abs().max()).item() < 1e-5
+    R = mk((M, N), 5)
+    Cb = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    T.gemm(T.BF16, M, N, K, A.data_ptr(), M, False, B.data_ptr(), N, False, Cb.data_ptr(), N, R=R.data_ptr())
+    torch.cuda.synchronize()
+    ref2 = ref + R.float()
+    assert ((Cb.float() - ref2).abs().max() / ref2.abs().max()).item() < 1e-2
+
+
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, False)])
+def test_simt_gemm_fp32(T, a_k, b_k):
+    M, N, K = 96, 80, 72
+    A = mk((M, K) if a_k else (K, M), 6, torch.float32)
+    B = mk((N, K) if b_k else (K, N), 7, torch.float32)
+    C = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    T.gemm(T.FP32, M, N, K, A.data_ptr(), K if a_k else M, a_k, B.data_ptr(), K if b_k else N, b_k,
+           C.data_ptr(), N)
+    torch.cuda.synchronize()
+    Ad = A.double() if a_k else A.double().t()
+    Bd = B.double() if b_k else B.double().t()
+    ref = Ad @ Bd.t()
+    assert ((C.double() - ref).abs().max() / ref.abs().max()).item() < 1e-6
+
+
+def attn_case(B, S, nh, dh, seed, dtype):
+    rng = np.random.default_rng(seed)
+    H = nh * dh
+    qkv = rng.standard_normal((B * S, 3 * H)).astype(np.float32)
+    do = rng.standard_normal((B * S, H)).astype(np.float32)
+    tq = torch.tensor(qkv).to(dtype).cuda()
+    tdo = torch.tensor(do).to(dtype).cuda()
+    return tq, tdo
+
+
+def oracle_attention(tq, tdo, B, S, nh, dh):
+    qkv = tq.double().cpu().numpy()
+    do = tdo.double().cpu().numpy()
+    H = nh * dh
+    outs = []
+    for b in range(B):
+        r = slice(b * S, (b + 1) * S)
+        q = qkv[r, :H].reshape(S, nh, dh)
+        k = qkv[r, H:2 * H].reshape(S, nh, dh)
+        v = qkv[r, 2 * H:].reshape(S, nh, dh)
+        o, P = om.attention_fwd(q, k, v)
+        dq, dk, dv = om.attention_bwd(do[r].reshape(S, nh, dh), q, k, v, o, P)
+        # LSE from the definition
+        c = 1.0 / np.sqrt(dh)
+        lse = np.empty((nh, S))
+        for h in range(nh):
+            s = c * q[:, h] @ k[:, h].T
+            s[np.triu(np.ones((S, S), bool), 1)] = -np.inf
+            mx = s.max(1)
+            lse[h] = mx + np.log(np.exp(s - mx[:, None]).sum(1))
+        outs.append((o.reshape(S, H), lse, np.concatenate([dq.reshape(S, H), dk.reshape(S, H),
+                                                           dv.reshape(S, H)], 1)))
+    return (np.concatenate([x[0] for x in outs]), np.stack([x[1] for x in outs]),
+            np.concatenate([x[2] for x in outs]))
+
+
+def run_attention(T, dtype_code, tq, tdo, B, S, nh, dh):
+    H = nh * dh
+    tdt = tq.dtype
+    o = torch.empty((B * S, H), dtype=tdt, device="cuda")
+    lse = torch.empty((B, nh, S), dtype=torch.float32, device="cuda")
+    T.attention_fwd(dtype_code, B, S, nh, dh, tq.data_ptr(), o.data_ptr(), lse.data_ptr())
+    dqkv = torch.empty_like(tq)
+    delta = torch.empty((B, nh, S), dtype=torch.float32, device="cuda")
+    dq_acc = torch.empty((B * S, H), dtype=torch.float32, device="cuda")
+    T.attention_bwd(dtype_code, B, S, nh, dh, tq.data_ptr(), o.data_ptr(), lse.data_ptr(), tdo.data_ptr(),
+                    dqkv.data_ptr(), delta.data_ptr(), dq_acc.data_ptr())
+    torch.cuda.synchronize()
+    return o.double().cpu().numpy(), lse.double().cpu().numpy(), dqkv.double().cpu().numpy()
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+@pytest.mark.parametrize("B,S,nh,dh", [(1, 128, 4, 16), (2, 200, 2, 32), (1, 256, 2, 128)])
+def test_attention_fp32_matches_oracle(T, B, S, nh, dh):
+    tq, tdo = attn_case(B, S, nh, dh, 11, torch.float32)
+    o, lse, dqkv = run_attention(T, T.FP32, tq, tdo, B, S, nh, dh)
+    ro, rl, rd = oracle_attention(tq, tdo, B, S, nh, dh)
+    assert rel(o, ro) < 1e-5 and rel(lse, rl) < 1e-5 and rel(dqkv, rd) < 1e-4
+
+
+@pytest.mark.parametrize("B,S,nh,dh", [(1, 128, 2, 64), (1, 384, 2, 128), (2, 256, 3, 128), (1, 1024, 1, 128),
+                                      (1, 4096, 2, 128)])
+def test_attention_bf16_matches_oracle(T, B, S, nh, dh):
+    tq, tdo = attn_case(B, S, nh, dh, 12, torch.bfloat16)
+    o, lse, dqkv = run_attention(T, T.BF16, tq, tdo, B, S, nh, dh)
+    ro, rl, rd = oracle_attention(tq, tdo, B, S, nh, dh)
+    assert rel(o, ro) < 2e-2 and rel(lse, rl) < 1e-2 and rel(dqkv, rd) < 3e-2, (rel(o, ro), rel(lse, rl),
+                                                                              rel(dqkv, rd))

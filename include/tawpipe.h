@@ -88,6 +88,14 @@ int tawpipe_bootstrap(int rank, int world, int device, const void* unique_id);
  * Returns 0, TAWPIPE_ECONFIG (message names the violated constraint) or TAWPIPE_ERUNTIME. */
 int tawpipe_init(int n_devices, int group_size, int n_layers, const tawpipe_dims* dims, int n_micro);
 
+/* Host-only dry run of the DBS plan for device `rank` (no GPU, no communication): validates the
+ * configuration exactly like tawpipe_init (world size taken = n_devices), and returns the byte ledger one
+ * tawpipe_step would record on that rank (same order as tawpipe_ledger; NULL to skip) and the number of
+ * elements tawpipe_shard would write (NULL to skip).  The ledger is produced by the same accounting code
+ * the real communication calls use.  LOCAL.  Returns 0 or TAWPIPE_ECONFIG. */
+int tawpipe_plan(int n_devices, int group_size, int n_layers, const tawpipe_dims* dims, int n_micro, int rank,
+                 uint64_t* ledger_out, int64_t* shard_elems_out);
+
 /* Load the full model (host fp32, canonical layout, n_elems = V·H + L·φ + H + V·H with
  * φ = 4H²+3HI+2H): [E | layer 0 .. layer L−1 | γ_f | W_head], each layer
  * [attn_norm | Wq | Wk | Wv | Wo | mlp_norm | Wgate | Wup | Wdown], matrices row-major

@@ -256,8 +256,31 @@ void k_rope(void* qkv, bool inverse, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------ comm (a3, a8)
-void ledger_add(int kind, int cls, int dir, int unit, int64_t n) {
-  g->ledger[ledger_index(kind, cls, dir, unit)] += static_cast<uint64_t>(n);
+// Logical-element ledger of one gather / one reduction of unit u on device (k, j):
+// all-gather and reduce-scatter: (G-1)·s received and sent per participant; P2P: s per message.
+void ledger_gather(const Unit& u, int G, int D, uint64_t* led) {
+  if (D > 1) {
+    if (u.owned)
+      led[ledger_index(K_W, C_INTER, D_SENT, u.cls)] += static_cast<uint64_t>(u.s) * (D - 1);
+    else
+      led[ledger_index(K_W, C_INTER, D_RECV, u.cls)] += static_cast<uint64_t>(u.s);
+  }
+  if (G > 1) {
+    led[ledger_index(K_W, C_INTRA, D_RECV, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
+    led[ledger_index(K_W, C_INTRA, D_SENT, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
+  }
+}
+void ledger_reduce(const Unit& u, int G, int D, uint64_t* led) {
+  if (G > 1) {
+    led[ledger_index(K_G, C_INTRA, D_RECV, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
+    led[ledger_index(K_G, C_INTRA, D_SENT, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
+  }
+  if (D > 1) {
+    if (u.owned)
+      led[ledger_index(K_G, C_INTER, D_RECV, u.cls)] += static_cast<uint64_t>(u.s) * (D - 1);
+    else
+      led[ledger_index(K_G, C_INTER, D_SENT, u.cls)] += static_cast<uint64_t>(u.s);
+  }
 }
 
 // full unit buffer the compute reads for unit u (slot for layers)
@@ -272,7 +295,7 @@ void* unit_buffer(int uid, int slot) {
 // a3: rail P2P of stripe j from the owner group (if remote) + intra-group all-gather, on ws
 void gather(int uid, void* dst) {
   const Unit& u = g->units[uid];
-  if (g->G == 1 && u.owned) return;
+  if (g->P == 1) return;  // nothing to move; the compute reads the owned copy in place
   Timed t(g->ws, 5, 0);
   void* own = wptr(g->wire, u.off);
   if (g->D > 1) {
@@ -280,19 +303,16 @@ void gather(int uid, void* dst) {
     if (u.owned) {
       for (int kk = 0; kk < g->D; ++kk)
         if (kk != g->k) TP_NCCL(ncclSend(own, u.s, wire_type(), kk, g->wr, g->ws));
-      ledger_add(K_W, C_INTER, D_SENT, u.cls, u.s * (g->D - 1));
     } else {
       TP_NCCL(ncclRecv(wptr(dst, g->j * u.s), u.s, wire_type(), u.owner, g->wr, g->ws));
-      ledger_add(K_W, C_INTER, D_RECV, u.cls, u.s);
     }
     TP_NCCL(ncclGroupEnd());
   }
   if (g->G > 1) {
     const void* send = u.owned ? own : wptr(dst, g->j * u.s);
     TP_NCCL(ncclAllGather(send, dst, u.s, wire_type(), g->wg, g->ws));
-    ledger_add(K_W, C_INTRA, D_RECV, u.cls, u.s * (g->G - 1));
-    ledger_add(K_W, C_INTRA, D_SENT, u.cls, u.s * (g->G - 1));
   }
+  ledger_gather(u, g->G, g->D, g->ledger);
 }
 
 // a8 + a9: reduce-scatter in the group, rail P2P to the owner, ascending-k accumulate + AdamW, on gs
@@ -310,8 +330,6 @@ void reduce_and_update(int uid, float* gacc) {
   if (g->G > 1) {
     Timed t(s, 5, 0);
     TP_NCCL(ncclReduceScatter(g->gwire, g->rsout, u.s, wire_type(), ncclSum, g->gg, s));
-    ledger_add(K_G, C_INTRA, D_RECV, u.cls, u.s * (g->G - 1));
-    ledger_add(K_G, C_INTRA, D_SENT, u.cls, u.s * (g->G - 1));
     own_partial = g->rsout;
   }
   if (g->D > 1) {
@@ -321,13 +339,12 @@ void reduce_and_update(int uid, float* gacc) {
       int idx = 0;
       for (int kk = 0; kk < g->D; ++kk)
         if (kk != g->k) TP_NCCL(ncclRecv(wptr(g->crecv, (idx++) * u.s), u.s, wire_type(), kk, g->gr, s));
-      ledger_add(K_G, C_INTER, D_RECV, u.cls, u.s * (g->D - 1));
     } else {
       TP_NCCL(ncclSend(own_partial, u.s, wire_type(), u.owner, g->gr, s));
-      ledger_add(K_G, C_INTER, D_SENT, u.cls, u.s);
     }
     TP_NCCL(ncclGroupEnd());
   }
+  ledger_reduce(u, g->G, g->D, g->ledger);
   if (!u.owned) return;
   const void* contrib[8];
   int idx = 0;
@@ -629,11 +646,10 @@ int64_t pad_to(int64_t n, int G) {
   return q * ((n + q - 1) / q);
 }
 
-void build(int P, int G, int L, const tawpipe_dims* d, int N) {
-  Ctx& c = *g;
+void validate(int P, int G, int L, const tawpipe_dims* d, int N, int world) {
   TP_CHECK(d != nullptr, TAWPIPE_ECONFIG, "dims is NULL");
-  TP_CHECK(P == c.world, TAWPIPE_ECONFIG, "n_devices (" + std::to_string(P) + ") != world size (" +
-                                              std::to_string(c.world) + ")");
+  TP_CHECK(P == world, TAWPIPE_ECONFIG, "n_devices (" + std::to_string(P) + ") != world size (" +
+                                            std::to_string(world) + ")");
   TP_CHECK(G >= 1 && P % G == 0, TAWPIPE_ECONFIG, "P mod G != 0 (PAPER.md:53 requires P mod D = 0)");
   const int D = P / G;
   TP_CHECK(L >= 1 && L % D == 0, TAWPIPE_ECONFIG, "L mod D != 0 (striped DBS, reading R6)");
@@ -651,6 +667,62 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
     TP_CHECK(d->hidden % 128 == 0 && d->ffn % 128 == 0 && d->vocab % 128 == 0, TAWPIPE_ECONFIG,
              "bf16 path: H, I, V must be multiples of 128");
   }
+}
+
+// DBS plan (a1): units, ownership, stripes, canonical offsets, owned-state offsets of rank (k, j)
+struct Plan {
+  std::vector<Unit> units;
+  int64_t owned_total = 0, max_pad = 0, max_s = 0;
+};
+Plan make_plan(int P, int G, int L, int64_t H, int64_t I, int64_t V, int rank) {
+  Plan pl;
+  const int D = P / G, k = rank / G;
+  const int64_t phi = 4 * H * H + 3 * H * I + 2 * H;
+  pl.units.assign(L + 2, Unit{});
+  for (int l = 0; l < L + 2; ++l) {
+    Unit& u = pl.units[l];
+    if (l < L) {
+      u.cls = U_BLOCK;
+      u.n = phi;
+      u.owner = l % D;
+      u.canon = V * H + static_cast<int64_t>(l) * phi;
+      u.n_nd = 2;  // RMSNorm gains: no weight decay (R1)
+      u.nd_lo[0] = 0;
+      u.nd_hi[0] = H;
+      u.nd_lo[1] = H + 4 * H * H;
+      u.nd_hi[1] = 2 * H + 4 * H * H;
+    } else if (l == L) {
+      u.cls = U_E;
+      u.n = V * H;
+      u.owner = 0;
+      u.canon = 0;
+    } else {
+      u.cls = U_F;
+      u.n = H + V * H;
+      u.owner = D - 1;
+      u.canon = V * H + static_cast<int64_t>(L) * phi;
+      u.n_nd = 1;
+      u.nd_lo[0] = 0;
+      u.nd_hi[0] = H;
+    }
+    u.n_pad = pad_to(u.n, G);
+    u.s = u.n_pad / G;
+    u.owned = (u.owner == k);
+    pl.max_pad = std::max(pl.max_pad, u.n_pad);
+    pl.max_s = std::max(pl.max_s, u.s);
+  }
+  for (int l = 0; l < L + 2; ++l)  // canonical shard order: layers ascending, then E, then F
+    if (pl.units[l].owned) {
+      pl.units[l].off = pl.owned_total;
+      pl.owned_total += pl.units[l].s;
+    }
+  return pl;
+}
+
+void build(int P, int G, int L, const tawpipe_dims* d, int N) {
+  Ctx& c = *g;
+  validate(P, G, L, d, N, c.world);
+  const int D = P / G;
   c.P = P;
   c.G = G;
   c.D = D;
@@ -672,46 +744,13 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   c.esz = c.bf ? 2 : 4;
   const int64_t H = c.H, I = c.I, V = c.V;
   c.phi = 4 * H * H + 3 * H * I + 2 * H;
-  // ---- DBS plan (a1): units, ownership, stripes, canonical offsets, owned-state offsets
-  c.units.assign(L + 2, Unit{});
-  for (int l = 0; l < L + 2; ++l) {
-    Unit& u = c.units[l];
-    if (l < L) {
-      u.cls = U_BLOCK;
-      u.n = c.phi;
-      u.owner = l % D;
-      u.canon = V * H + static_cast<int64_t>(l) * c.phi;
-      u.n_nd = 2;  // RMSNorm gains: no weight decay (R1)
-      u.nd_lo[0] = 0;
-      u.nd_hi[0] = H;
-      u.nd_lo[1] = H + 4 * H * H;
-      u.nd_hi[1] = 2 * H + 4 * H * H;
-    } else if (l == L) {
-      u.cls = U_E;
-      u.n = V * H;
-      u.owner = 0;
-      u.canon = 0;
-    } else {
-      u.cls = U_F;
-      u.n = H + V * H;
-      u.owner = D - 1;
-      u.canon = V * H + static_cast<int64_t>(L) * c.phi;
-      u.n_nd = 1;
-      u.nd_lo[0] = 0;
-      u.nd_hi[0] = H;
-    }
-    u.n_pad = pad_to(u.n, G);
-    u.s = u.n_pad / G;
-    u.owned = (u.owner == c.k);
-    c.max_pad = std::max(c.max_pad, u.n_pad);
-    c.max_s = std::max(c.max_s, u.s);
+  {
+    Plan pl = make_plan(P, G, L, H, I, V, c.rank);
+    c.units = pl.units;
+    c.owned_total = pl.owned_total;
+    c.max_pad = pl.max_pad;
+    c.max_s = pl.max_s;
   }
-  c.owned_total = 0;
-  for (int l = 0; l < L + 2; ++l)  // canonical shard order: layers ascending, then E, then F
-    if (c.units[l].owned) {
-      c.units[l].off = c.owned_total;
-      c.owned_total += c.units[l].s;
-    }
   // ---- streams, events, communicators
   TP_CUDA(cudaStreamCreateWithFlags(&c.cs, cudaStreamNonBlocking));
   TP_CUDA(cudaStreamCreateWithFlags(&c.ws, cudaStreamNonBlocking));
@@ -924,6 +963,30 @@ int tawpipe_bootstrap(int rank, int world, int device, const void* uid) {
       TP_NCCL(ncclCommInitRank(&g->world_comm, world, id, rank));
     }
     g->booted = true;
+  });
+}
+
+int tawpipe_plan(int n_devices, int group_size, int n_layers, const tawpipe_dims* dims, int n_micro, int rank,
+                 uint64_t* ledger_out, int64_t* shard_elems_out) {
+  return guarded([&] {
+    validate(n_devices, group_size, n_layers, dims, n_micro, n_devices);
+    TP_CHECK(rank >= 0 && rank < n_devices, TAWPIPE_ECONFIG, "rank out of range");
+    const int G = group_size, D = n_devices / group_size, L = n_layers;
+    Plan pl = make_plan(n_devices, G, L, dims->hidden, dims->ffn, dims->vocab, rank);
+    uint64_t led[TAWPIPE_LEDGER_N] = {};
+    // the step's communication sequence (run_step): E gather, forward gathers 0..L-1, F gather, F reduction,
+    // backward gathers L-2..0 (layer L-1 reuses its forward buffer, R12) with reductions L-1..0, E reduction
+    ledger_gather(pl.units[L], G, D, led);
+    for (int l = 0; l < L; ++l) ledger_gather(pl.units[l], G, D, led);
+    ledger_gather(pl.units[L + 1], G, D, led);
+    ledger_reduce(pl.units[L + 1], G, D, led);
+    for (int l = L - 1; l >= 0; --l) {
+      if (l != L - 1) ledger_gather(pl.units[l], G, D, led);
+      ledger_reduce(pl.units[l], G, D, led);
+    }
+    ledger_reduce(pl.units[L], G, D, led);
+    if (ledger_out) std::memcpy(ledger_out, led, sizeof(led));
+    if (shard_elems_out) *shard_elems_out = pl.owned_total;
   });
 }
 

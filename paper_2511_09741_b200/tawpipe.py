@@ -60,6 +60,7 @@ def lib():
         "tawpipe_get_unique_id": (i32, [vp]),
         "tawpipe_bootstrap": (i32, [i32, i32, i32, vp]),
         "tawpipe_init": (i32, [i32, i32, i32, ctypes.POINTER(Dims), i32]),
+        "tawpipe_plan": (i32, [i32, i32, i32, ctypes.POINTER(Dims), i32, i32, vp, vp]),
         "tawpipe_load": (i32, [vp, i64]),
         "tawpipe_step": (f32, [vp]),
         "tawpipe_step_device": (f32, [vp]),
@@ -146,6 +147,19 @@ def dist_env():
     return rank, world, local
 
 
+def share_unique_id(rank: int, world: int, pg_backend: str = "gloo") -> bytes:
+    """Rank 0 creates the NCCL unique id; torch.distributed broadcasts its 128 bytes to every rank."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        dist.init_process_group(backend=pg_backend, rank=rank, world_size=world)
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        t = torch.tensor(list(unique_id()), dtype=torch.uint8)
+    dist.broadcast(t, src=0)
+    return bytes(t.tolist())
+
+
 def bootstrap(rank=None, world=None, device=None, pg_backend="gloo"):
     """Bind to the GPU and build the world NCCL communicator.  For world > 1 the 128-byte NCCL unique id is
     broadcast from rank 0 with torch.distributed (plumbing only)."""
@@ -153,17 +167,7 @@ def bootstrap(rank=None, world=None, device=None, pg_backend="gloo"):
     rank = r if rank is None else rank
     world = w if world is None else world
     device = loc if device is None else device
-    uid = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        if not dist.is_initialized():
-            dist.init_process_group(backend=pg_backend, rank=rank, world_size=world)
-        t = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            t = torch.tensor(list(unique_id()), dtype=torch.uint8)
-        dist.broadcast(t, src=0)
-        uid = bytes(t.tolist())
+    uid = share_unique_id(rank, world, pg_backend) if world > 1 else None
     buf = ctypes.create_string_buffer(uid, 128) if uid is not None else None
     _check(lib().tawpipe_bootstrap(rank, world, device, buf))
     return rank, world, device
@@ -224,6 +228,16 @@ class Session:
 
     def close(self):
         lib().tawpipe_finalize()
+
+
+def plan(n_devices: int, group_size: int, dims: ModelDims, n_micro: int, rank: int):
+    """Host-only dry run (tawpipe_plan): (ledger list, shard elements) of `rank`; raises on invalid config."""
+    led = (ctypes.c_uint64 * LEDGER_N)()
+    n = ctypes.c_int64(0)
+    cd = dims.to_c()
+    _check(lib().tawpipe_plan(n_devices, group_size, dims.n_layers, ctypes.byref(cd), n_micro, rank, led,
+                              ctypes.byref(n)))
+    return [int(x) for x in led], int(n.value)
 
 
 # ---------------------------------------------------------------------------------------------- kernel-level

@@ -1,0 +1,77 @@
+"""Multi-GPU parity of the GWPS/DBS/CCO step (one process per GPU over NCCL, launched with torchrun):
+losses and updated weights vs the fp64 oracle's single-device step, and every rank's byte ledger vs the
+closed forms of SURVEY.md App. A (bit-exact).  Runs only when the box has >= P GPUs
+(gpurun --gpus 2 / --gpus 4)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from helpers import C0, C0B, ROOT, om, oracle_cfg, reassemble, weight_errors
+from oracle import layout as OL
+from oracle import ledger as LG
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+# (name, base dims, P, G, L, N, dtype, ckpt, no_cco)
+CASES = [
+    ("c0-1x2-fsdp", C0, 2, 2, 2, 4, 0, 0, False),
+    ("c0-2x1-p2p", C0, 2, 1, 2, 4, 0, 0, False),
+    ("c0-2x2", C0, 4, 2, 2, 4, 0, 0, False),          # BASELINE.json configs[0]
+    ("c0-2x2-nocco", C0, 4, 2, 2, 4, 0, 0, True),
+    ("c0-1x4", C0, 4, 4, 2, 8, 0, 1, False),
+    ("c0-4x1", C0, 4, 1, 4, 4, 0, 0, False),
+    ("c0b-2x2-bf16", C0B, 4, 2, 2, 4, 1, 1, False),
+    ("c0b-1x2-bf16", C0B, 2, 2, 2, 2, 1, 0, False),
+]
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco", CASES, ids=[c[0] for c in CASES])
+def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    cfg = oracle_cfg(base, n_layers=L)
+    steps = 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
+           "--cfg", json.dumps(dict(base, n_layers=L)), "--G", str(G), "--N", str(N), "--steps", str(steps),
+           "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else [])
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
+    # oracle: plain single-device step on the same tokens
+    params = synth.perturb_gains(synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab))
+    st = om.init_state(params)
+    theta0 = om.to_f64(params)
+    grads = []
+    tol_loss, tol_w, kappa = (1e-5, 1e-4, 1e-3) if dtype == 0 else (1e-2, 2e-2, 5e-2)
+    for step in range(steps):
+        toks = synth.tokens(N, cfg.micro_bs, cfg.seq, cfg.vocab, step=step)
+        lr, g = om.train_step(st, toks, cfg)
+        grads.append(g)
+        for i in range(P):   # identical loss on every rank
+            assert abs(res[i]["losses"][step] - lr) / lr <= tol_loss, (i, step, res[i]["losses"][step], lr)
+        if step == 0:
+            theta1 = {k: v for k, v in st.params.items()}
+    gpu = reassemble(cfg, P, G, [x["shard"] for x in res])
+    et, ed, viol, off, rep = weight_errors(gpu, st.params, theta0, grads, cfg, kappa)
+    assert et <= tol_w and viol == 0, (et, viol, sorted(rep, key=lambda z: -z[1])[:3])
+    # byte ledger: bit-exact against the closed forms, every rank, every step
+    H, V = cfg.hidden, cfg.vocab
+    s, e, f = (OL.padded(n, G) // G for n in (om.phi(cfg), V * H, H + V * H))
+    for i in range(P):
+        expect = LG.closed_form(L, P, G, i // G, s, e, f, r=1)
+        for step in range(steps):
+            assert [int(x) for x in res[i]["ledgers"][step]] == expect, (i, step)

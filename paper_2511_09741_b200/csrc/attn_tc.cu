@@ -260,29 +260,38 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // =============================================================================================== backward
+// Warp roles (320 threads, one CTA per SM):
+//   warps 0-3  softmax-gradient warps, thread t <-> key row t of the tile (TMEM lane t):
+//              Pᵀ = exp2(Sᵀ·c·log2e − LSE·log2e) is written back into TMEM as packed bf16 over Sᵀ's columns
+//              (the A operand of dV += Pᵀ·dO), dSᵀ = Pᵀ⊙(dPᵀ − δ) goes to smem (A of dK, MN-major A of dQ)
+//   warps 4-7  dQ warps: read dQ_i (TMEM lanes = query rows) and reduce it into the fp32 accumulator
+//   warp 8     TMA producer (K, V once; Q_i and dO_i double-buffered)
+//   warp 9     MMA issuer: Sᵀ, dPᵀ, dV += Pᵀ·dO, dK += dSᵀ·Q, dQ_i = dS·K (into dPᵀ's TMEM columns)
 template <int DH>
 struct BwdSmem {
   static constexpr int QB = DH / 64 * ATOM;
-  static constexpr int OFF_K = 0, OFF_V = QB, OFF_Q = 2 * QB, OFF_DO = 3 * QB;
-  static constexpr int OFF_P = 4 * QB;           // Pᵀ  [kv][q], 2 atoms
-  static constexpr int OFF_DS = OFF_P + 2 * ATOM;  // dSᵀ [kv][q], 2 atoms
-  static constexpr int OFF_LSE = OFF_DS + 2 * ATOM;  // 2 × 128 floats (double-buffered)
-  static constexpr int OFF_DEL = OFF_LSE + 1024;
+  static constexpr int OFF_K = 0, OFF_V = QB, OFF_Q = 2 * QB, OFF_DO = 4 * QB;  // Q, dO: 2 stages each
+  static constexpr int OFF_DS = 6 * QB;              // dSᵀ [kv][q], 2 atoms
+  static constexpr int OFF_LSE = OFF_DS + 2 * ATOM;  // 2 × 128 floats
+  static constexpr int OFF_DEL = OFF_LSE + 1024;     // 2 × 128 floats
   static constexpr int OFF_BAR = OFF_DEL + 1024;
-  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+  static constexpr int BYTES = OFF_BAR + 256;
 };
 
+__device__ __forceinline__ float bf_lo(uint32_t x) { return __uint_as_float(x << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
+
 template <int DH>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
                   const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                   bf16* __restrict__ dqkv, int S, int nh, float scale, float scale2) {
   using L = BwdSmem<DH>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 2, *s_full = bar + 3, *dp_full = bar + 4,
-           *ds_full = bar + 5, *mma2_done = bar + 6, *dq_free = bar + 7;
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *s_full = bar + 5, *dp_full = bar + 6,
+           *tdp_free = bar + 7, *p_ready = bar + 8, *ds_ready = bar + 9, *mm2_done = bar + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
   float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
   float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
@@ -297,26 +306,30 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   if (threadIdx.x == 0) {
+    if (smem_u32(sm) & 1023) __trap();  // SW128 tiles need a 1024-byte aligned base
     tma_prefetch(&tm);
     tma_prefetch(&tmdo);
     mbar_init(kv_full, 1);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(ds_full, 128);
-    mbar_init(mma2_done, 1);
-    mbar_init(dq_free, 128);
+    mbar_init(tdp_free, 128);
+    mbar_init(p_ready, 128);
+    mbar_init(ds_ready, 128);
+    mbar_init(mm2_done, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
 
-  if (warp == 0) {
+  if (warp == 8) {
     if (lane == 0) {
       mbar_expect_tx(kv_full, 2 * L::QB);
       for (int a = 0; a < DH / 64; ++a) {
@@ -324,53 +337,54 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d(sm + L::OFF_V + a * ATOM, &tm, kv_full, 2 * H + h * DH + a * 64, row0 + jt * BQ);
       }
       for (int it = 0; it < n_it; ++it) {
-        const int i = jt + it;
-        mbar_wait(q_empty, (it & 1) ^ 1);
-        mbar_expect_tx(q_full, 2 * L::QB);
+        const int i = jt + it, st = it & 1;
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * L::QB);
         for (int a = 0; a < DH / 64; ++a) {
-          tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + i * BQ);
-          tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, q_full, h * DH + a * 64, row0 + i * BQ);
+          tma_load_2d(sm + L::OFF_Q + st * L::QB + a * ATOM, &tm, &q_full[st], h * DH + a * 64, row0 + i * BQ);
+          tma_load_2d(sm + L::OFF_DO + st * L::QB + a * ATOM, &tmdo, &q_full[st], h * DH + a * 64, row0 + i * BQ);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     if (lane == 0) {
-      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);    // Sᵀ, dPᵀ: K-major A and B (K = d)
-      constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);     // dV, dK: A K-major (K = q), B MN-major
-      constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);       // dQ: A = dSᵀ viewed MN-major, B MN-major
-      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sQ = smem_u32(sm + L::OFF_Q),
-                     sDO = smem_u32(sm + L::OFF_DO), sP = smem_u32(sm + L::OFF_P), sDS = smem_u32(sm + L::OFF_DS);
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
+      constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
+      constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
+      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS);
       mbar_wait(kv_full, 0);
       for (int it = 0; it < n_it; ++it) {
-        mbar_wait(q_full, it & 1);
-        if (it > 0) mbar_wait(dq_free, (it - 1) & 1);
+        const int st = it & 1;
+        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB), sDO = smem_u32(sm + L::OFF_DO + st * L::QB);
+        mbar_wait(&q_full[st], (it >> 1) & 1);
         tc_fence_after();
+        // tS held Pᵀ_{it-1}, read by the softmax warps before ds_ready(it-1), which was awaited below
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
         umma_commit(s_full);
+        if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
+        tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
         umma_commit(dp_full);
-        mbar_wait(ds_full, it & 1);
+        mbar_wait(p_ready, it & 1);
         tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) {
-          umma_f16(tdV, desc_k(sP, ks), desc_mn(sDO, ks), id_kv, (it | ks) > 0);
-          umma_f16(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
-        }
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
+        mbar_wait(ds_ready, it & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tS, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
-        umma_commit(q_empty);
-        umma_commit(mma2_done);
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
+        umma_commit(&q_empty[st]);
+        umma_commit(mm2_done);
       }
     }
-  } else {
-    const int q = warp & 3;
-    const int t = q * 32 + lane;   // TMEM lane: key row (Sᵀ, dPᵀ, dK, dV) or query row (dQ)
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* sP = sm + L::OFF_P;
+  } else if (warp < 4) {
+    const int t = warp * 32 + lane;  // key row of the tile (TMEM lane)
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     uint8_t* sDS = sm + L::OFF_DS;
-    float p[128];
     for (int it = 0; it < n_it; ++it) {
       const int i = jt + it;
       const int buf = it & 1;
@@ -379,70 +393,68 @@ __global__ void __launch_bounds__(192, 1)
       del_s[buf * 128 + t] = delta[li];
       named_bar(1, 128);
       const float* ls = lse_s + buf * 128;
-      const float* ds_ = del_s + buf * 128;
+      const float* dl = del_s + buf * 128;
       mbar_wait(s_full, it & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t u[32];
+        uint32_t u[32], pw[16];
         tmem_ld32(tS + lane_off + c * 32, u);
         tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 32; ++k) p[c * 32 + k] = ex2(__uint_as_float(u[k]) * scale2 - ls[c * 32 + k]);
+        for (int k = 0; k < 32; k += 2) {
+          float p0 = ex2(__uint_as_float(u[k]) * scale2 - ls[c * 32 + k]);
+          float p1 = ex2(__uint_as_float(u[k + 1]) * scale2 - ls[c * 32 + k + 1]);
+          if (it == 0) {  // diagonal tile: query index < key index is masked
+            if (c * 32 + k < t) p0 = 0.f;
+            if (c * 32 + k + 1 < t) p1 = 0.f;
+          }
+          pw[k / 2] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < (c+1)*32)
       }
-      if (it == 0) {  // diagonal tile: query index < key index is masked
-#pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if (k < t) p[k] = 0.f;
-      }
-      if (it > 0) mbar_wait(mma2_done, (it - 1) & 1);  // Pᵀ / dSᵀ smem of the previous iteration consumed
-      store_row_sw128(sP, t, p);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_ready);
       mbar_wait(dp_full, it & 1);
+      if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ smem of the previous tile consumed
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t u[32];
+        uint32_t u[32], pw[16];
         tmem_ld32(tdP + lane_off + c * 32, u);
+        tmem_ld16(tS + lane_off + c * 16, pw);
         tmem_wait_ld();
+        uint32_t d[16];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) p[c * 32 + k] = p[c * 32 + k] * (__uint_as_float(u[k]) - ds_[c * 32 + k]);
+        for (int k = 0; k < 32; k += 2)
+          d[k / 2] = pack_bf16(bf_lo(pw[k / 2]) * (__uint_as_float(u[k]) - dl[c * 32 + k]),
+                               bf_hi(pw[k / 2]) * (__uint_as_float(u[k + 1]) - dl[c * 32 + k + 1]));
+        // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int chunk = (c & 1) * 4 + v;
+          *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
+              make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
+        }
       }
-      store_row_sw128(sDS, t, p);
       fence_async_smem();
       tc_fence_before();
-      mbar_arrive(ds_full);
-      // dQ_i rows (TMEM lane = query row t of tile i) -> fp32 accumulator
-      mbar_wait(mma2_done, it & 1);
-      tc_fence_after();
-      float* dq = dq_acc + static_cast<int64_t>(row0 + i * BQ + t) * H + h * DH;
-#pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tS + lane_off + c * 32, u);
-        tmem_wait_ld();
-#pragma unroll
-        for (int v = 0; v < 8; ++v)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 32 + v * 4),
-                       "f"(__uint_as_float(u[4 * v])), "f"(__uint_as_float(u[4 * v + 1])),
-                       "f"(__uint_as_float(u[4 * v + 2])), "f"(__uint_as_float(u[4 * v + 3]))
-                       : "memory");
-      }
-      tc_fence_before();
-      mbar_arrive(dq_free);
+      mbar_arrive(ds_ready);
     }
     // dK (× softmax scale) and dV rows of this key tile
-    mbar_wait(mma2_done, (n_it - 1) & 1);
+    mbar_wait(mm2_done, (n_it - 1) & 1);
     tc_fence_after();
-    bf16* dk = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + H + h * DH;
-    bf16* dv = dk + H;
+    bf16* dkp = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + H + h * DH;
+    bf16* dvp = dkp + H;
 #pragma unroll 1
     for (int c = 0; c < DH / 32; ++c) {
       uint32_t u[32], w[32];
       tmem_ld32(tdK + lane_off + c * 32, u);
       tmem_ld32(tdV + lane_off + c * 32, w);
       tmem_wait_ld();
-      uint4* k4 = reinterpret_cast<uint4*>(dk + c * 32);
-      uint4* v4 = reinterpret_cast<uint4*>(dv + c * 32);
+      uint4* k4 = reinterpret_cast<uint4*>(dkp + c * 32);
+      uint4* v4 = reinterpret_cast<uint4*>(dvp + c * 32);
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         uint4 o, o2;
@@ -459,9 +471,34 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     tc_fence_before();
+  } else if (warp < 8) {
+    // dQ warps 4-7: TMEM lane quarter (warp % 4) holds query rows of dQ_i
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    for (int it = 0; it < n_it; ++it) {
+      const int i = jt + it;
+      mbar_wait(mm2_done, it & 1);
+      tc_fence_after();
+      float* dq = dq_acc + static_cast<int64_t>(row0 + i * BQ + t) * H + h * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tdP + lane_off + c * 32, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 32 + v * 4),
+                       "f"(__uint_as_float(u[4 * v])), "f"(__uint_as_float(u[4 * v + 1])),
+                       "f"(__uint_as_float(u[4 * v + 2])), "f"(__uint_as_float(u[4 * v + 3]))
+                       : "memory");
+      }
+      tc_fence_before();
+      mbar_arrive(tdp_free);
+    }
   }
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -548,13 +585,26 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   if (dh == 128) {
     static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<128><<<grid, 192, BwdSmem<128>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
                                                                scale2);
   } else {
     static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<64><<<grid, 192, BwdSmem<64>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
                                                              scale2);
+  }
+  {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFuncAttributes a{};
+      if (dh == 128) cudaFuncGetAttributes(&a, fa_bwd_kernel<128>);
+      else cudaFuncGetAttributes(&a, fa_bwd_kernel<64>);
+      throw Error(TAWPIPE_ERUNTIME, std::string("fa_bwd launch: ") + cudaGetErrorString(e) + " regs " +
+                                        std::to_string(a.numRegs) + " maxThreads " + std::to_string(a.maxThreadsPerBlock) +
+                                        " static smem " + std::to_string(a.sharedSizeBytes) + " max dyn " +
+                                        std::to_string(a.maxDynamicSharedSizeBytes) + " requested dyn " +
+                                        std::to_string(dh == 128 ? BwdSmem<128>::BYTES : BwdSmem<64>::BYTES));
+    }
   }
   fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
   TP_CUDA(cudaGetLastError());

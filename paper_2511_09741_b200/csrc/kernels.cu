@@ -2,6 +2,8 @@
 // initialisation and the fused gradient-accumulate + AdamW update on the owned DBS stripe.
 // Formulas: SURVEY.md §8(c) (forward algorithm and backward-formula table); AdamW: PyTorch semantics (R1).
 // All reductions run in fp32 regardless of the storage type T (float or bf16).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace tp {
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const T* __restrict__ d
 }
 
 // ------------------------------------------------------------------------------------ RoPE (rotate-half)
-// qkv rows of width ncols_blocks·H? No: rows are [q | k | v] of width 3H; blocks 0 (q) and 1 (k) are rotated.
+// rows are [q | k | v] of width 3H; column blocks 0 (q) and 1 (k) are rotated.
 template <typename T>
 __global__ void rope_kernel(T* __restrict__ qkv, int64_t rows, int S, int nh, int dh, int64_t ld,
                             const float* __restrict__ cs, const float* __restrict__ sn, int inverse, int nblk) {
@@ -291,6 +293,167 @@ __global__ void adamw_kernel(Contribs c, int n_contrib, int own_k, int own_f32, 
   }
 }
 
+// ------------------------------------------------------------------------------------ bf16 vectorised variants
+// 16-byte accesses (8 bf16 per thread), no 64-bit index division in the inner loop.
+__device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(h[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void st8(bf16* p, const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// grid (rows), block = nblk·nh·(half/8) threads (<= 1024): each thread rotates 8 pairs of one head
+__global__ void rope_v8_kernel(bf16* __restrict__ qkv, int S, int nh, int dh, int64_t ld, const float* __restrict__ cs,
+                               const float* __restrict__ sn, int inverse) {
+  const int64_t row = blockIdx.x;
+  const int p = static_cast<int>(row % S);
+  const int half = dh / 2, per_head = half / 8;
+  const int t = threadIdx.x;
+  const int head = t / per_head;          // over nblk·nh
+  const int i0 = (t % per_head) * 8;
+  bf16* base = qkv + row * ld + static_cast<int64_t>(head) * dh;
+  float x1[8], x2[8], c[8], sv[8];
+  ld8(base + i0, x1);
+  ld8(base + i0 + half, x2);
+  const float4* c4 = reinterpret_cast<const float4*>(cs + static_cast<int64_t>(p) * half + i0);
+  const float4* s4 = reinterpret_cast<const float4*>(sn + static_cast<int64_t>(p) * half + i0);
+  *reinterpret_cast<float4*>(c) = c4[0];
+  *reinterpret_cast<float4*>(c + 4) = c4[1];
+  *reinterpret_cast<float4*>(sv) = s4[0];
+  *reinterpret_cast<float4*>(sv + 4) = s4[1];
+  float y1[8], y2[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float sk = inverse ? -sv[k] : sv[k];
+    y1[k] = x1[k] * c[k] - x2[k] * sk;
+    y2[k] = x2[k] * c[k] + x1[k] * sk;
+  }
+  st8(base + i0, y1);
+  st8(base + i0 + half, y2);
+}
+
+// grid (ceil(I/8/256), rows)
+__global__ void swiglu_fwd_v8_kernel(const bf16* __restrict__ gu, bf16* __restrict__ y, int I) {
+  const int64_t r = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= I) return;
+  float u[8], w[8], o[8];
+  ld8(gu + r * 2 * I + c, u);
+  ld8(gu + r * 2 * I + I + c, w);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o[k] = u[k] * sigmoidf_(u[k]) * w[k];
+  st8(y + r * I + c, o);
+}
+
+__global__ void swiglu_bwd_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ gu, bf16* __restrict__ dgu,
+                                     int I) {
+  const int64_t r = blockIdx.y;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= I) return;
+  float u[8], w[8], d[8], du[8], dw[8];
+  ld8(gu + r * 2 * I + c, u);
+  ld8(gu + r * 2 * I + I + c, w);
+  ld8(dy + r * I + c, d);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float sg = sigmoidf_(u[k]);
+    du[k] = d[k] * w[k] * sg * (1.f + u[k] * (1.f - sg));
+    dw[k] = d[k] * u[k] * sg;
+  }
+  st8(dgu + r * 2 * I + c, du);
+  st8(dgu + r * 2 * I + I + c, dw);
+}
+
+// one warp per row, H % 256 == 0 (each lane: H/256 vectors of 8)
+template <int NV>
+__global__ void rmsnorm_fwd_v8_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g, bf16* __restrict__ y,
+                                      float* __restrict__ rstd, int64_t rows, int H, float eps) {
+  const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  float v[NV][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    ld8(x + row * H + (i * 32 + lane) * 8, v[i]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss += v[i][k] * v[i][k];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float r = rsqrtf(ss / H + eps);
+  if (lane == 0) rstd[row] = r;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float gg[8], o8[8];
+    ld8(g + (i * 32 + lane) * 8, gg);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o8[k] = v[i][k] * r * gg[k];
+    st8(y + row * H + (i * 32 + lane) * 8, o8);
+  }
+}
+
+// one warp per row (RW rows per warp for the dγ partial sums, then one atomicAdd per column per warp)
+template <int NV, int RW>
+__global__ void rmsnorm_bwd_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                      const bf16* __restrict__ g, const float* __restrict__ rstd,
+                                      const bf16* __restrict__ res, bf16* __restrict__ dx, float* __restrict__ dg_acc,
+                                      int64_t rows, int H) {
+  const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  float dg[NV][8];
+  float gv[NV][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    ld8(g + (i * 32 + lane) * 8, gv[i]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dg[i][k] = 0.f;
+  }
+  for (int rr = 0; rr < RW; ++rr) {
+    const int64_t row = w * RW + rr;
+    if (row >= rows) break;
+    const float r = rstd[row];
+    float d[NV][8], xv[NV][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      ld8(dy + row * H + (i * 32 + lane) * 8, d[i]);
+      ld8(x + row * H + (i * 32 + lane) * 8, xv[i]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        dot += d[i][k] * gv[i][k] * xv[i][k];
+        dg[i][k] += d[i][k] * xv[i][k] * r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float coef = r * r * r * dot / H;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float o8[8], rs[8];
+      if (res) ld8(res + row * H + (i * 32 + lane) * 8, rs);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) o8[k] = r * d[i][k] * gv[i][k] - xv[i][k] * coef + (res ? rs[k] : 0.f);
+      st8(dx + row * H + (i * 32 + lane) * 8, o8);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(&dg_acc[(i * 32 + lane) * 8 + k], dg[i][k]);
+}
+
 inline unsigned grid_stride_blocks(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -316,12 +479,35 @@ void embed_bwd(const int32_t* tok, int64_t stride_seq, int B, int S, const void*
 }
 template <typename T>
 void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
+    switch (H) {
+      case 256: rmsnorm_fwd_v8_kernel<1><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
+      case 1024: rmsnorm_fwd_v8_kernel<4><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
+      case 2048: rmsnorm_fwd_v8_kernel<8><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
+      case 4096: rmsnorm_fwd_v8_kernel<16><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
+      case 5120: rmsnorm_fwd_v8_kernel<20><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
+      default: break;
+    }
+  }
   rmsnorm_fwd_kernel<T, 256><<<static_cast<unsigned>(rows), 256, 0, s>>>(x, g, y, rstd, H, eps);
   LAUNCHED();
 }
 template <typename T>
 void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
                  int64_t rows, int H, cudaStream_t s) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    constexpr int RW = 16;  // rows per warp
+    const unsigned blocks = static_cast<unsigned>((rows + 8 * RW - 1) / (8 * RW));
+    switch (H) {
+      case 256: rmsnorm_bwd_v8_kernel<1, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
+      case 1024: rmsnorm_bwd_v8_kernel<4, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
+      case 2048: rmsnorm_bwd_v8_kernel<8, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
+      case 4096: rmsnorm_bwd_v8_kernel<16, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
+      case 5120: rmsnorm_bwd_v8_kernel<20, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
+      default: break;
+    }
+  }
   constexpr int RB = 32;
   const size_t smem = static_cast<size_t>(H) * sizeof(float);
   if (smem > 48 * 1024) {
@@ -335,6 +521,15 @@ template <typename T>
 void rope_apply(T* qkv, int B, int S, int nh, int dh, const float* cs, const float* sn, bool inverse, int nblk,
                 cudaStream_t s) {
   const int64_t rows = static_cast<int64_t>(B) * S;
+  if constexpr (std::is_same<T, bf16>::value) {
+    const int threads = nblk * nh * (dh / 2 / 8);
+    if ((dh / 2) % 8 == 0 && threads <= 1024) {
+      rope_v8_kernel<<<static_cast<unsigned>(rows), threads, 0, s>>>(qkv, S, nh, dh, 3ll * nh * dh, cs, sn,
+                                                                      inverse ? 1 : 0);
+      LAUNCHED();
+      return;
+    }
+  }
   const int64_t total = rows * nblk * nh * (dh / 2);
   rope_kernel<T><<<grid_stride_blocks(total), 256, 0, s>>>(qkv, rows, S, nh, dh, 3ll * nh * dh, cs, sn,
                                                           inverse ? 1 : 0, nblk);
@@ -342,11 +537,25 @@ void rope_apply(T* qkv, int B, int S, int nh, int dh, const float* cs, const flo
 }
 template <typename T>
 void swiglu_fwd(const T* gu, T* y, int64_t rows, int I, cudaStream_t s) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (I % 8 == 0 && rows <= 65535) {
+      swiglu_fwd_v8_kernel<<<dim3((I / 8 + 255) / 256, static_cast<unsigned>(rows)), 256, 0, s>>>(gu, y, I);
+      LAUNCHED();
+      return;
+    }
+  }
   swiglu_fwd_kernel<T><<<grid_stride_blocks(rows * I), 256, 0, s>>>(gu, y, rows, I);
   LAUNCHED();
 }
 template <typename T>
 void swiglu_bwd(const T* dy, const T* gu, T* dgu, int64_t rows, int I, cudaStream_t s) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (I % 8 == 0 && rows <= 65535) {
+      swiglu_bwd_v8_kernel<<<dim3((I / 8 + 255) / 256, static_cast<unsigned>(rows)), 256, 0, s>>>(dy, gu, dgu, I);
+      LAUNCHED();
+      return;
+    }
+  }
   swiglu_bwd_kernel<T><<<grid_stride_blocks(rows * I), 256, 0, s>>>(dy, gu, dgu, rows, I);
   LAUNCHED();
 }

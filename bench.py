@@ -256,6 +256,14 @@ def run_ours(args, c):
     step_roof_ms = max(flops_per_token(c) * c["m"] * c["B"] * c["S"] / (peaks["bf16_tflops"] * 1e12) * 1e3,
                        max(sum(ledger[i] for i in range(24) if (i // 3) % 2 == 0),
                            sum(ledger[i] for i in range(24) if (i // 3) % 2 == 1)) * wire / 770e9 * 1e3)
+    wsz = 2 if c["dtype"] == 1 else 4
+    w_bytes = sum(ledger[i] for i in range(24) if i < 12 and (i // 3) % 2 == 0) * wsz   # weight elements received
+    g_bytes = sum(ledger[i] for i in range(24) if i >= 12 and (i // 3) % 2 == 0) * wsz  # grad elements received
+    comm = {"weight_gather": {"ms": st["weight_comm_ms"], "bytes_recv": w_bytes,
+                              "gbs": w_bytes / max(st["weight_comm_ms"], 1e-9) / 1e6},
+            "grad_reduce": {"ms": st["grad_comm_ms"], "bytes_recv": g_bytes,
+                            "gbs": g_bytes / max(st["grad_comm_ms"], 1e-9) / 1e6},
+            "exposed_ms": exposed, "overlapped_ms": max(0.0, st["weight_comm_ms"] + st["grad_comm_ms"] - exposed)}
     out = {
         "metric": METRIC, "value": tokens_step / (ms / 1e3), "unit": "tokens/s",
         "tokens_per_s_per_gpu": tokens_step / (ms / 1e3) / world,
@@ -266,7 +274,7 @@ def run_ours(args, c):
                    "seq_len": c["S"], "parallelism": f"tawpipe {world // G}x{G} (D x G)",
                    "l2": "inputs and weights far larger than L2 (no flush needed)",
                    "schedule": "no-CCO ablation" if args.no_cco else "GWPS+DBS+CCO"},
-        "exposed_comm_ms": exposed, "exposed_comm_frac": exposed / ms,
+        "exposed_comm_ms": exposed, "exposed_comm_frac": exposed / ms, "comm": comm,
         "step_roofline_frac": step_roof_ms / ms,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": ach / peak, "traffic": None,

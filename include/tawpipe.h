@@ -131,7 +131,7 @@ int tawpipe_ledger(uint64_t* out, int n);
 
 /* Timing of the last step (requires tawpipe_set_timing(1) before it), n >= TAWPIPE_STATS_N:
  *  [0] step ms (compute stream, event to event)      [1] exposed-comm ms (compute-stream waits)
- *  [2] weight-comm ms (wstream busy)                 [3] grad-comm+AdamW ms (gstream busy)
+ *  [2] weight-comm ms (sum of gather P2P+all-gather) [3] grad-comm ms (sum of reduce-scatter + P2P)
  *  [4] GEMM ms (sum of tcgen05/SIMT GEMM launches)   [5] GEMM algorithmic GFLOP
  *  [6] GEMM launches                                 [7] attention ms   [8] attention GFLOP
  *  [9] AdamW ms   [10] AdamW algorithmic GB          [11] kernel launches in the step

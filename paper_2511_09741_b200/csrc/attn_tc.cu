@@ -12,12 +12,15 @@
 // as a K-major operand (Q, K for QKᵀ) and as an MN-major operand (V, dO, Q, K in the PV / gradient products).
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace tp {
 
 CUtensorMap make_tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer);
+CUtensorMap make_tmap_f32_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer);
 
 namespace {
 
@@ -30,6 +33,19 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 2^x on the FMA/ALU pipes (offloads the MUFU unit, which is the softmax bottleneck at d_h = 128):
+// x = n + f with n = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3 minimax polynomial (max rel. error 1.0e-4,
+// below bf16 rounding of P); 2^n added to the exponent field.  Valid for x in [-126, 0] (softmax arguments).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: rounds x to the nearest integer in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.0550089308f, f, 0.242210984f), f, 0.69328293f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+// element k of a 32-wide chunk: emulate 3 of every 8 exponentials on the FMA pipe
+__device__ __forceinline__ float ex2_mix(float x, int k) { return ex2(x); }  // emulation off: measured slower (r01)
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -219,7 +235,7 @@ __global__ void __launch_bounds__(192, 1)
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
-        const float p = ex2(s[i] - m2);
+        const float p = ex2_mix(s[i] - m2, i);
         s[i] = p;
         sum += p;
       }
@@ -259,19 +275,458 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ----------------------------------------------------------------------------------------------- forward v2
+// Two 128-row query tiles per CTA (A = tile 2t, B = tile 2t+1) with one softmax warpgroup each, so that the
+// exp work of one tile overlaps the tensor-core work of the other (ping-pong); P is written back into its
+// S columns of TMEM as packed bf16 and read from there as the A operand of O += P·V.
+//   warps 0-3: softmax A, warps 4-7: softmax B, warp 8: TMA producer, warp 9: MMA issuer (+ TMEM owner)
+//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
+template <int DH>
+struct Fwd2Smem {
+  static constexpr int QB = DH / 64 * ATOM;
+  static constexpr int OFF_Q = 0;        // Q_A, Q_B
+  static constexpr int OFF_K = 2 * QB;   // 2 stages
+  static constexpr int OFF_V = 4 * QB;   // 2 stages
+  static constexpr int OFF_BAR = 6 * QB;
+  static constexpr int BYTES = OFF_BAR + 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(320, 1)
+    fa_fwd2_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
+                   int nh, float scale2) {
+  using L = Fwd2Smem<DH>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
+           *s_full = bar + 9, *p_ready = bar + 11, *o_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int n_q = S / BQ;
+  const int n_pair = (n_q + 1) / 2;
+  const int t = n_pair - 1 - static_cast<int>(blockIdx.x / nh);  // heaviest pairs first
+  const int h = blockIdx.x % nh;
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int qa = 2 * t, qb = 2 * t + 1;
+  const bool hasB = qb < n_q;
+  const int n_kv = hasB ? qb + 1 : qa + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_ready[i], 128);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, (hasB ? 2 : 1) * L::QB);
+      for (int a = 0; a < DH / 64; ++a) {
+        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qa * BQ);
+        if (hasB) tma_load_2d(sm + L::OFF_Q + L::QB + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qb * BQ);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
+                      row0 + j * BQ);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
+      const uint32_t sQ[2] = {smem_u32(sm + L::OFF_Q), smem_u32(sm + L::OFF_Q + L::QB)};
+      auto issue_s = [&](int w, int j) {
+        const uint32_t sK = smem_u32(sm + L::OFF_K + (j & 1) * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_f16(tmem + w * 128, desc_k(sQ[w], ks), desc_k(sK, ks), id_qk, ks > 0);
+        umma_commit(&s_full[w]);
+      };
+      auto issue_pv = [&](int w, int j) {
+        const uint32_t sV = smem_u32(sm + L::OFF_V + (j & 1) * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          umma_f16_tmemA(tmem + 256 + w * 128, tmem + w * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
+        umma_commit(&o_done[w]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      if (hasB) issue_s(1, 0);
+      umma_commit(&k_empty[0]);
+      for (int j = 0; j < n_kv; ++j) {
+        const bool actA = j <= qa;
+        const bool next = j + 1 < n_kv;
+        if (next) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        if (actA) {
+          mbar_wait(&p_ready[0], j & 1);
+          tc_fence_after();
+          issue_pv(0, j);
+          if (j + 1 <= qa) issue_s(0, j + 1);
+        }
+        if (hasB) {
+          mbar_wait(&p_ready[1], j & 1);
+          tc_fence_after();
+          issue_pv(1, j);
+          if (next) issue_s(1, j + 1);
+        }
+        umma_commit(&v_empty[j & 1]);
+        if (next) umma_commit(&k_empty[(j + 1) & 1]);
+      }
+    }
+  } else {
+    const int w = warp >> 2;        // 0: tile A, 1: tile B
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int qt = w == 0 ? qa : qb;
+    if (w == 0 || hasB) {
+      const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+      const uint32_t tS = tmem + w * 128, tO = tmem + 256 + w * 128;
+      float m2 = -INFINITY, l = 0.f;
+      for (int j = 0; j <= qt; ++j) {
+        const bool diag = (j == qt);
+        mbar_wait(&s_full[w], j & 1);
+        tc_fence_after();
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32];
+          tmem_ld32(tS + lane_off + c * 32, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float v = (diag && c * 32 + k > r) ? -INFINITY : __uint_as_float(u[k]) * scale2;
+            mx = fmaxf(mx, v);
+          }
+        }
+        if (j == 0) {
+          m2 = mx;
+        } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
+          // lazy rescale of O (stable: PV_{j-1} completed before S_j was committed, in issue order)
+          const float mnew = fmaxf(m2, mx);
+          const float alpha = ex2(m2 - mnew);
+          l *= alpha;
+#pragma unroll 1
+          for (int c = 0; c < DH / 32; ++c) {
+            uint32_t u[32];
+            tmem_ld32(tO + lane_off + c * 32, u);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) u[k] = __float_as_uint(__uint_as_float(u[k]) * alpha);
+            tmem_st32(tO + lane_off + c * 32, u);
+          }
+          m2 = mnew;
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t u[32], pw[16];
+          tmem_ld32(tS + lane_off + c * 32, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            float p0 = ex2_mix(__uint_as_float(u[k]) * scale2 - m2, k);
+            float p1 = ex2_mix(__uint_as_float(u[k + 1]) * scale2 - m2, k + 1);
+            if (diag) {
+              if (c * 32 + k > r) p0 = 0.f;
+              if (c * 32 + k + 1 > r) p1 = 0.f;
+            }
+            sum += p0 + p1;
+            pw[k / 2] = pack_bf16(p0, p1);
+          }
+          tmem_st16(tS + lane_off + c * 16, pw);  // P over S columns already read
+        }
+        l += sum;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_ready[w]);
+      }
+      mbar_wait(&o_done[w], qt & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tO + lane_off + c * 32, u);
+        tmem_wait_ld();
+        uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 o;
+          o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+          o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+          o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+          o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+          d4[v] = o;
+        }
+      }
+      lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
+      tc_fence_before();
+    }
+  }
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ----------------------------------------------------------------------------------------------- forward v3
+// One 128-row query tile per CTA; S double-buffered in TMEM, P written back over its S columns (packed bf16)
+// and consumed from TMEM as the A operand of O += P·V.  The softmax of tile j therefore never waits for the
+// P·V of tile j−1 except when the running max grows by more than 2^8 and O must be rescaled (lazy rescale):
+// the exp work overlaps P·V_{j−1} and S_{j+1} on the tensor core.
+//   warp 0: TMA producer (Q once; K, V in 3-stage rings), warp 1: MMA issuer, warps 2-5: softmax
+//   TMEM: S0 [0,128) S1 [128,256) O [256,384)
+template <int DH>
+struct Fwd3Smem {
+  static constexpr int QB = DH / 64 * ATOM;
+  static constexpr int NST = 3;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = QB;
+  static constexpr int OFF_V = QB + NST * QB;
+  static constexpr int OFF_BAR = QB + 2 * NST * QB;
+  static constexpr int BYTES = OFF_BAR + 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(192, 1)
+    fa_fwd3_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
+                   int nh, float scale2) {
+  using L = Fwd3Smem<DH>;
+  constexpr int NST = L::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
+           *v_empty = bar + 1 + 3 * NST, *s_full = bar + 1 + 4 * NST, *p_ready = bar + 3 + 4 * NST,
+           *o_done = bar + 5 + 4 * NST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8 + 4 * NST);
+
+  const int n_q = S / BQ;
+  const int qt = n_q - 1 - static_cast<int>(blockIdx.x / nh);  // heaviest tiles first
+  const int h = blockIdx.x % nh;
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int n_kv = qt + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_ready[i], 128);
+    }
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, L::QB);
+      for (int a = 0; a < DH / 64; ++a)
+        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qt * BQ);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % NST;
+        const uint32_t ph = (j / NST) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
+                      row0 + j * BQ);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
+      const uint32_t sQ = smem_u32(sm + L::OFF_Q);
+      auto issue_s = [&](int j) {
+        const int st = j % NST;
+        mbar_wait(&k_full[st], (j / NST) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tmem + (j & 1) * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[j & 1]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (n_kv > 1) issue_s(1);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % NST;
+        mbar_wait(&p_ready[j & 1], (j >> 1) & 1);
+        mbar_wait(&v_full[st], (j / NST) & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          umma_f16_tmemA(tO, tmem + (j & 1) * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
+        umma_commit(&v_empty[st]);
+        umma_commit(o_done);
+        if (j + 2 < n_kv) issue_s(j + 2);   // overwrites S/P buffer (j & 1) after P·V_j in issue order
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    float m2 = -INFINITY, l = 0.f;
+    float s[128];
+    for (int j = 0; j < n_kv; ++j) {
+      const uint32_t tS = tmem + (j & 1) * 128 + lane_off;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tS + c * 32, u);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]);
+      }
+      if (j == qt) {  // diagonal tile only
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > r) s[i] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      mx *= scale2;
+      if (j == 0) {
+        m2 = mx;
+      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
+        // rescale O: needs P·V_{j-1} complete (the only place the softmax waits for the tensor core)
+        mbar_wait(o_done, (j - 1) & 1);
+        tc_fence_after();
+        const float mnew = fmaxf(m2, mx);
+        const float alpha = ex2(m2 - mnew);
+        l *= alpha;
+#pragma unroll 1
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld32(tO + lane_off + c * 32, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st32(tO + lane_off + c * 32, u);
+        }
+        m2 = mnew;
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pw[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2_mix(fmaf(s[c * 32 + i], scale2, -m2), i);
+          const float p1 = ex2_mix(fmaf(s[c * 32 + i + 1], scale2, -m2), i + 1);
+          sum += p0 + p1;
+          pw[i / 2] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + c * 16, pw);
+      }
+      l += sum;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_ready[j & 1]);
+    }
+    mbar_wait(o_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tO + lane_off + c * 32, u);
+      tmem_wait_ld();
+      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 o;
+        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+        d4[v] = o;
+      }
+    }
+    lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // =============================================================================================== backward
 // Warp roles (320 threads, one CTA per SM):
 //   warps 0-3  softmax-gradient warps, thread t <-> key row t of the tile (TMEM lane t):
 //              Pᵀ = exp2(Sᵀ·c·log2e − LSE·log2e) is written back into TMEM as packed bf16 over Sᵀ's columns
 //              (the A operand of dV += Pᵀ·dO), dSᵀ = Pᵀ⊙(dPᵀ − δ) goes to smem (A of dK, MN-major A of dQ)
-//   warps 4-7  dQ warps: read dQ_i (TMEM lanes = query rows) and reduce it into the fp32 accumulator
-//   warp 8     TMA producer (K, V once; Q_i and dO_i double-buffered)
+//   warps 4-7  dQ warps: read dQ_i (TMEM lanes = query rows), stage it (fp32, 128-byte swizzle) in the dSᵀ
+//              buffer once the MMAs have consumed dSᵀ, and add it into the fp32 accumulator with TMA
+//              tensor reduce-add (cp.reduce.async.bulk.tensor)
+//   warp 8     TMA producer (K, V once; Q_i, dO_i, LSE_i, δ_i double-buffered)
 //   warp 9     MMA issuer: Sᵀ, dPᵀ, dV += Pᵀ·dO, dK += dSᵀ·Q, dQ_i = dS·K (into dPᵀ's TMEM columns)
 template <int DH>
 struct BwdSmem {
   static constexpr int QB = DH / 64 * ATOM;
   static constexpr int OFF_K = 0, OFF_V = QB, OFF_Q = 2 * QB, OFF_DO = 4 * QB;  // Q, dO: 2 stages each
-  static constexpr int OFF_DS = 6 * QB;              // dSᵀ [kv][q], 2 atoms
+  static constexpr int OFF_DS = 6 * QB;              // dSᵀ [kv][q], 2 atoms; then dQ staging (2 × 16 KB fp32)
   static constexpr int OFF_LSE = OFF_DS + 2 * ATOM;  // 2 × 128 floats
   static constexpr int OFF_DEL = OFF_LSE + 1024;     // 2 × 128 floats
   static constexpr int OFF_BAR = OFF_DEL + 1024;
@@ -284,14 +739,15 @@ __device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 
 template <int DH>
 __global__ void __launch_bounds__(320, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
-                  const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
+                  const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                   bf16* __restrict__ dqkv, int S, int nh, float scale, float scale2) {
   using L = BwdSmem<DH>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *s_full = bar + 5, *dp_full = bar + 6,
-           *tdp_free = bar + 7, *p_ready = bar + 8, *ds_ready = bar + 9, *mm2_done = bar + 10;
+           *tdp_free = bar + 7, *p_ready = bar + 8, *ds_ready = bar + 9, *mm2_done = bar + 10,
+           *dsbuf_free = bar + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
   float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
   float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
@@ -320,6 +776,7 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(p_ready, 128);
     mbar_init(ds_ready, 128);
     mbar_init(mm2_done, 1);
+    mbar_init(dsbuf_free, 1);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -339,11 +796,14 @@ __global__ void __launch_bounds__(320, 1)
       for (int it = 0; it < n_it; ++it) {
         const int i = jt + it, st = it & 1;
         mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * L::QB);
+        mbar_expect_tx(&q_full[st], 2 * L::QB + 1024);
         for (int a = 0; a < DH / 64; ++a) {
           tma_load_2d(sm + L::OFF_Q + st * L::QB + a * ATOM, &tm, &q_full[st], h * DH + a * 64, row0 + i * BQ);
           tma_load_2d(sm + L::OFF_DO + st * L::QB + a * ATOM, &tmdo, &q_full[st], h * DH + a * 64, row0 + i * BQ);
         }
+        const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ;
+        bulk_load(lse_s + st * 128, lse + li, 512, &q_full[st]);
+        bulk_load(del_s + st * 128, delta + li, 512, &q_full[st]);
       }
     }
   } else if (warp == 9) {
@@ -386,14 +846,8 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     uint8_t* sDS = sm + L::OFF_DS;
     for (int it = 0; it < n_it; ++it) {
-      const int i = jt + it;
-      const int buf = it & 1;
-      const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ + t;
-      lse_s[buf * 128 + t] = lse[li] * LOG2E;
-      del_s[buf * 128 + t] = delta[li];
-      named_bar(1, 128);
-      const float* ls = lse_s + buf * 128;
-      const float* dl = del_s + buf * 128;
+      const float* ls = lse_s + (it & 1) * 128;   // filled by the producer with Q_i (q_full[it & 1])
+      const float* dl = del_s + (it & 1) * 128;
       mbar_wait(s_full, it & 1);
       tc_fence_after();
 #pragma unroll
@@ -403,8 +857,8 @@ __global__ void __launch_bounds__(320, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
-          float p0 = ex2(__uint_as_float(u[k]) * scale2 - ls[c * 32 + k]);
-          float p1 = ex2(__uint_as_float(u[k + 1]) * scale2 - ls[c * 32 + k + 1]);
+          float p0 = ex2_mix(fmaf(__uint_as_float(u[k]), scale2, -ls[c * 32 + k] * LOG2E), k);
+          float p1 = ex2_mix(fmaf(__uint_as_float(u[k + 1]), scale2, -ls[c * 32 + k + 1] * LOG2E), k + 1);
           if (it == 0) {  // diagonal tile: query index < key index is masked
             if (c * 32 + k < t) p0 = 0.f;
             if (c * 32 + k + 1 < t) p1 = 0.f;
@@ -417,7 +871,7 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       mbar_arrive(p_ready);
       mbar_wait(dp_full, it & 1);
-      if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ smem of the previous tile consumed
+      if (it > 0) mbar_wait(dsbuf_free, (it - 1) & 1);  // dSᵀ buffer: MMAs and the dQ staging of it-1 done
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -476,26 +930,46 @@ __global__ void __launch_bounds__(320, 1)
     const int q = warp & 3;
     const int t = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sm + L::OFF_DS;
     for (int it = 0; it < n_it; ++it) {
       const int i = jt + it;
-      mbar_wait(mm2_done, it & 1);
+      mbar_wait(mm2_done, it & 1);   // dQ_i complete; dSᵀ consumed by the MMAs
       tc_fence_after();
-      float* dq = dq_acc + static_cast<int64_t>(row0 + i * BQ + t) * H + h * DH;
 #pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tdP + lane_off + c * 32, u);
+      for (int rd = 0; rd < DH / 64; ++rd) {
+        uint32_t u0[32], u1[32];
+        tmem_ld32(tdP + lane_off + rd * 64, u0);
+        tmem_ld32(tdP + lane_off + rd * 64 + 32, u1);
         tmem_wait_ld();
+        if (rd == DH / 64 - 1) {
+          tc_fence_before();
+          mbar_arrive(tdp_free);
+        }
+        if (rd > 0) {                          // staging reused: previous reduce must have read it
+          if (t == 0) bulk_wait_read0();
+          named_bar(2, 128);
+        }
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dq + c * 32 + v * 4),
-                       "f"(__uint_as_float(u[4 * v])), "f"(__uint_as_float(u[4 * v + 1])),
-                       "f"(__uint_as_float(u[4 * v + 2])), "f"(__uint_as_float(u[4 * v + 3]))
-                       : "memory");
+        for (int j = 0; j < 8; ++j) {
+          *reinterpret_cast<uint4*>(stg + t * 128 + ((j ^ (t & 7)) << 4)) =
+              make_uint4(u0[4 * j], u0[4 * j + 1], u0[4 * j + 2], u0[4 * j + 3]);
+          *reinterpret_cast<uint4*>(stg + ATOM + t * 128 + ((j ^ (t & 7)) << 4)) =
+              make_uint4(u1[4 * j], u1[4 * j + 1], u1[4 * j + 2], u1[4 * j + 3]);
+        }
+        fence_async_smem();
+        named_bar(2, 128);
+        if (t == 0) {
+          tma_reduce_add_2d(&tmdq, stg, h * DH + rd * 64, row0 + i * BQ);
+          tma_reduce_add_2d(&tmdq, stg + ATOM, h * DH + rd * 64 + 32, row0 + i * BQ);
+          bulk_commit();
+        }
       }
-      tc_fence_before();
-      mbar_arrive(tdp_free);
+      if (t == 0) {
+        bulk_wait_read0();
+        mbar_arrive(dsbuf_free);
+      }
     }
+    if (t == 0) bulk_wait_all0();
   }
   __syncthreads();
   if (warp == 9) {
@@ -554,6 +1028,40 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
   const int H = nh * dh;
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, static_cast<int64_t>(B) * S, 3ll * H, 128);
   const float scale2 = LOG2E / sqrtf(static_cast<float>(dh));
+  static const int fwd_ver = [] {
+    const char* e = std::getenv("TAWPIPE_FA_FWD");
+    return e ? std::atoi(e) : 3;
+  }();
+  if (fwd_ver == 3) {
+    dim3 grid3(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+    if (dh == 128) {
+      static bool once = (prep(fa_fwd3_kernel<128>, Fwd3Smem<128>::BYTES), true);
+      (void)once;
+      fa_fwd3_kernel<128><<<grid3, 192, Fwd3Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    } else {
+      static bool once = (prep(fa_fwd3_kernel<64>, Fwd3Smem<64>::BYTES), true);
+      (void)once;
+      fa_fwd3_kernel<64><<<grid3, 192, Fwd3Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    }
+    TP_CUDA(cudaGetLastError());
+    g_kstats.launches++;
+    return;
+  }
+  if (fwd_ver == 2) {
+    dim3 grid2(static_cast<unsigned>(((S / BQ + 1) / 2) * nh), static_cast<unsigned>(B));
+    if (dh == 128) {
+      static bool once = (prep(fa_fwd2_kernel<128>, Fwd2Smem<128>::BYTES), true);
+      (void)once;
+      fa_fwd2_kernel<128><<<grid2, 320, Fwd2Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    } else {
+      static bool once = (prep(fa_fwd2_kernel<64>, Fwd2Smem<64>::BYTES), true);
+      (void)once;
+      fa_fwd2_kernel<64><<<grid2, 320, Fwd2Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    }
+    TP_CUDA(cudaGetLastError());
+    g_kstats.launches++;
+    return;
+  }
   dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
   if (dh == 128) {
     static bool once = (prep(fa_fwd_kernel<128>, FwdSmem<128>::BYTES), true);
@@ -579,18 +1087,19 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   TP_CUDA(cudaMemsetAsync(dq_acc, 0, rows * H * sizeof(float), s));
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, rows, 3ll * H, 128);
   CUtensorMap tmdo = make_tmap_bf16_2d(dout, H, rows, H, 128);
+  CUtensorMap tmdq = make_tmap_f32_2d(dq_acc, H, rows, H, 128);
   const float scale = 1.0f / sqrtf(static_cast<float>(dh));
   const float scale2 = LOG2E * scale;
   dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
   if (dh == 128) {
     static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse, delta, dq_acc, dqkv, S, nh, scale,
                                                                scale2);
   } else {
     static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, lse, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse, delta, dq_acc, dqkv, S, nh, scale,
                                                              scale2);
   }
   {

@@ -57,7 +57,7 @@ struct Acts {  // one (layer, micro-batch) forward's saved tensors
 
 struct TimedRegion {
   cudaEvent_t a, b;
-  int kind;  // 0 gemm, 1 attention, 2 adamw, 3 exposed wait, 4 elementwise
+  int kind;  // 0 gemm, 1 attention, 2 adamw, 3 exposed wait, 4 elementwise, 5 weight comm, 6 grad comm
   double work;
 };
 
@@ -328,12 +328,12 @@ void reduce_and_update(int uid, float* gacc) {
     own_f32 = false;
   }
   if (g->G > 1) {
-    Timed t(s, 5, 0);
+    Timed t(s, 6, 0);
     TP_NCCL(ncclReduceScatter(g->gwire, g->rsout, u.s, wire_type(), ncclSum, g->gg, s));
     own_partial = g->rsout;
   }
   if (g->D > 1) {
-    Timed t(s, 5, 0);
+    Timed t(s, 6, 0);
     TP_NCCL(ncclGroupStart());
     if (u.owned) {
       int idx = 0;
@@ -625,14 +625,10 @@ double run_step(const int32_t* tokens, bool device_tokens) {
         case 2: c.stats[9] += e; c.stats[10] += r.work * 1e-9; break;
         case 3: c.stats[1] += e; break;
         case 4: c.stats[14] += e; break;
-        case 5: break;
+        case 5: c.stats[2] += e; break;
+        case 6: c.stats[3] += e; break;
       }
     }
-    float wms = 0.f, gms = 0.f;
-    TP_CUDA(cudaEventElapsedTime(&wms, c.ev_ws0, c.ev_ws1));
-    TP_CUDA(cudaEventElapsedTime(&gms, c.ev_gs0, c.ev_gs1));
-    c.stats[2] = wms;
-    c.stats[3] = gms;
   }
   c.stats[11] = static_cast<double>(g_kstats.launches - c.launches_at_start);
   c.stats[12] = static_cast<double>(c.bytes_alloc) * 1e-9;

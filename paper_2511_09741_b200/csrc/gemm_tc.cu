@@ -256,6 +256,20 @@ CUtensorMap make_tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, in
   return m;
 }
 
+// 2-D fp32 tensor map, box 32 inner (128 B) × box_outer, 128-byte swizzle (used for TMA reduce-add)
+CUtensorMap make_tmap_f32_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
+  cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TP_CHECK(r == CUDA_SUCCESS, TAWPIPE_ERUNTIME, "cuTensorMapEncodeTiled (f32) failed: " + std::to_string((int)r));
+  return m;
+}
+
 namespace {
 
 int g_num_sms = 0;

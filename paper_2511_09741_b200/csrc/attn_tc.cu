@@ -102,8 +102,9 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int n_q = S / BQ;
-  const int qt = n_q - 1 - static_cast<int>(blockIdx.x / nh);  // heaviest tiles first
-  const int h = blockIdx.x % nh;
+  // head-major order (the K/V of one head stay in L2 across its query tiles), heaviest tiles first in a head
+  const int qt = n_q - 1 - static_cast<int>(blockIdx.x % n_q);
+  const int h = static_cast<int>(blockIdx.x / n_q);
   const int b = blockIdx.y;
   const int H = nh * DH;
   const int row0 = b * S;
@@ -305,8 +306,8 @@ __global__ void __launch_bounds__(320, 1)
 
   const int n_q = S / BQ;
   const int n_pair = (n_q + 1) / 2;
-  const int t = n_pair - 1 - static_cast<int>(blockIdx.x / nh);  // heaviest pairs first
-  const int h = blockIdx.x % nh;
+  const int t = n_pair - 1 - static_cast<int>(blockIdx.x % n_pair);  // head-major, heaviest pairs first
+  const int h = static_cast<int>(blockIdx.x / n_pair);
   const int b = blockIdx.y;
   const int H = nh * DH;
   const int row0 = b * S;
@@ -534,8 +535,9 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8 + 4 * NST);
 
   const int n_q = S / BQ;
-  const int qt = n_q - 1 - static_cast<int>(blockIdx.x / nh);  // heaviest tiles first
-  const int h = blockIdx.x % nh;
+  // head-major order (the K/V of one head stay in L2 across its query tiles), heaviest tiles first in a head
+  const int qt = n_q - 1 - static_cast<int>(blockIdx.x % n_q);
+  const int h = static_cast<int>(blockIdx.x / n_q);
   const int b = blockIdx.y;
   const int H = nh * DH;
   const int row0 = b * S;
@@ -753,8 +755,9 @@ __global__ void __launch_bounds__(320, 1)
   float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
 
   const int n_q = S / BQ;
-  const int jt = static_cast<int>(blockIdx.x / nh);  // heaviest key tiles (most query tiles) first
-  const int h = blockIdx.x % nh;
+  // head-major order (Q, dO of one head stay in L2), heaviest key tiles (most query tiles) first in a head
+  const int jt = static_cast<int>(blockIdx.x % n_q);
+  const int h = static_cast<int>(blockIdx.x / n_q);
   const int b = blockIdx.y;
   const int H = nh * DH;
   const int row0 = b * S;

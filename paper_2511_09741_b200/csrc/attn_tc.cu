@@ -12,6 +12,7 @@
 // as a K-major operand (Q, K for QKᵀ) and as an MN-major operand (V, dO, Q, K in the PV / gradient products).
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -520,7 +521,7 @@ struct Fwd3Smem {
   static constexpr int BYTES = OFF_BAR + 256;
 };
 
-template <int DH>
+template <int DH, int EMU>
 __global__ void __launch_bounds__(192, 1)
     fa_fwd3_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
                    int nh, float scale2) {
@@ -629,22 +630,34 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tS = tmem + (j & 1) * 128 + lane_off;
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tS + c * 32, u);
+      {  // all four loads in flight before one wait (one TMEM round trip per row)
+        uint32_t u0[32], u1[32], u2[32], u3[32];
+        tmem_ld32(tS, u0);
+        tmem_ld32(tS + 32, u1);
+        tmem_ld32(tS + 64, u2);
+        tmem_ld32(tS + 96, u3);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]);
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(u0[i]);
+          s[32 + i] = __uint_as_float(u1[i]);
+          s[64 + i] = __uint_as_float(u2[i]);
+          s[96 + i] = __uint_as_float(u3[i]);
+        }
       }
       if (j == qt) {  // diagonal tile only
 #pragma unroll
         for (int i = 0; i < 128; ++i)
           if (i > r) s[i] = -INFINITY;
       }
-      float mx = s[0];
+      // row max with 8 independent chains (one softmax warp per SMSP: latency is not hidden)
+      float mxa[8];
 #pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+      for (int k = 0; k < 8; ++k) mxa[k] = s[k];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
       mx *= scale2;
       if (j == 0) {
         m2 = mx;
@@ -666,20 +679,22 @@ __global__ void __launch_bounds__(192, 1)
         }
         m2 = mnew;
       }
-      float sum = 0.f;
+      float sa[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};   // 8 independent partial sums
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t pw[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2_mix(fmaf(s[c * 32 + i], scale2, -m2), i);
-          const float p1 = ex2_mix(fmaf(s[c * 32 + i + 1], scale2, -m2), i + 1);
-          sum += p0 + p1;
+          const float a0 = fmaf(s[c * 32 + i], scale2, -m2), a1 = fmaf(s[c * 32 + i + 1], scale2, -m2);
+          const float p0 = (EMU && ((i & 7) >= 8 - EMU)) ? ex2_poly(a0) : ex2(a0);
+          const float p1 = (EMU && (((i + 1) & 7) >= 8 - EMU)) ? ex2_poly(a1) : ex2(a1);
+          sa[i & 7] += p0;
+          sa[(i + 1) & 7] += p1;
           pw[i / 2] = pack_bf16(p0, p1);
         }
         tmem_st16(tS + c * 16, pw);
       }
-      l += sum;
+      l += ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_ready[j & 1]);
@@ -742,8 +757,14 @@ template <int DH>
 __global__ void __launch_bounds__(320, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
                   const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
-                  bf16* __restrict__ dqkv, int S, int nh, float scale, float scale2) {
+                  bf16* __restrict__ dqkv, int S, int nh, float scale, float scale2,
+                  unsigned long long* __restrict__ trace) {
   using L = BwdSmem<DH>;
+  // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
+  auto TR = [&](int it, int ev) {
+    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32)
+      trace[it * 16 + ev] = clock64();
+  };
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
@@ -825,16 +846,20 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
         umma_commit(s_full);
+        TR(it, 0);
         if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
+        TR(it, 1);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
         umma_commit(dp_full);
         mbar_wait(p_ready, it & 1);
+        TR(it, 2);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
         mbar_wait(ds_ready, it & 1);
+        TR(it, 3);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
@@ -852,52 +877,69 @@ __global__ void __launch_bounds__(320, 1)
       const float* ls = lse_s + (it & 1) * 128;   // filled by the producer with Q_i (q_full[it & 1])
       const float* dl = del_s + (it & 1) * 128;
       mbar_wait(s_full, it & 1);
+      if (t == 0) TR(it, 4);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t u[32], pw[16];
-        tmem_ld32(tS + lane_off + c * 32, u);
+      for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+        uint32_t uu[2][32];
+        tmem_ld32(tS + lane_off + cp * 32, uu[0]);
+        tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
         tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          float p0 = ex2_mix(fmaf(__uint_as_float(u[k]), scale2, -ls[c * 32 + k] * LOG2E), k);
-          float p1 = ex2_mix(fmaf(__uint_as_float(u[k + 1]), scale2, -ls[c * 32 + k + 1] * LOG2E), k + 1);
-          if (it == 0) {  // diagonal tile: query index < key index is masked
-            if (c * 32 + k < t) p0 = 0.f;
-            if (c * 32 + k + 1 < t) p1 = 0.f;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = cp + h2;
+          uint32_t pw[16];
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            float p0 = ex2_mix(fmaf(__uint_as_float(uu[h2][k]), scale2, -ls[c * 32 + k] * LOG2E), k);
+            float p1 = ex2_mix(fmaf(__uint_as_float(uu[h2][k + 1]), scale2, -ls[c * 32 + k + 1] * LOG2E), k + 1);
+            if (it == 0) {  // diagonal tile: query index < key index is masked
+              if (c * 32 + k < t) p0 = 0.f;
+              if (c * 32 + k + 1 < t) p1 = 0.f;
+            }
+            pw[k / 2] = pack_bf16(p0, p1);
           }
-          pw[k / 2] = pack_bf16(p0, p1);
+          tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < cp*32+64)
         }
-        tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < (c+1)*32)
       }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_ready);
+      if (t == 0) TR(it, 5);
       mbar_wait(dp_full, it & 1);
+      if (t == 0) TR(it, 6);
       if (it > 0) mbar_wait(dsbuf_free, (it - 1) & 1);  // dSᵀ buffer: MMAs and the dQ staging of it-1 done
+      if (t == 0) TR(it, 7);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t u[32], pw[16];
-        tmem_ld32(tdP + lane_off + c * 32, u);
-        tmem_ld16(tS + lane_off + c * 16, pw);
+      for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+        uint32_t uu[2][32], pp[2][16];
+        tmem_ld32(tdP + lane_off + cp * 32, uu[0]);
+        tmem_ld32(tdP + lane_off + cp * 32 + 32, uu[1]);
+        tmem_ld16(tS + lane_off + cp * 16, pp[0]);
+        tmem_ld16(tS + lane_off + cp * 16 + 16, pp[1]);
         tmem_wait_ld();
-        uint32_t d[16];
 #pragma unroll
-        for (int k = 0; k < 32; k += 2)
-          d[k / 2] = pack_bf16(bf_lo(pw[k / 2]) * (__uint_as_float(u[k]) - dl[c * 32 + k]),
-                               bf_hi(pw[k / 2]) * (__uint_as_float(u[k + 1]) - dl[c * 32 + k + 1]));
-        // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = cp + h2;
+          uint32_t d[16];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int chunk = (c & 1) * 4 + v;
-          *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
-              make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
+          for (int k = 0; k < 32; k += 2)
+            d[k / 2] = pack_bf16(bf_lo(pp[h2][k / 2]) * (__uint_as_float(uu[h2][k]) - dl[c * 32 + k]),
+                                 bf_hi(pp[h2][k / 2]) * (__uint_as_float(uu[h2][k + 1]) - dl[c * 32 + k + 1]));
+          // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int chunk = (c & 1) * 4 + v;
+            *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
+                make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
+          }
         }
       }
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(ds_ready);
+      if (t == 0) TR(it, 8);
     }
     // dK (× softmax scale) and dV rows of this key tile
     mbar_wait(mm2_done, (n_it - 1) & 1);
@@ -937,6 +979,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int it = 0; it < n_it; ++it) {
       const int i = jt + it;
       mbar_wait(mm2_done, it & 1);   // dQ_i complete; dSᵀ consumed by the MMAs
+      if (t == 0) TR(it, 9);
       tc_fence_after();
 #pragma unroll 1
       for (int rd = 0; rd < DH / 64; ++rd) {
@@ -947,6 +990,7 @@ __global__ void __launch_bounds__(320, 1)
         if (rd == DH / 64 - 1) {
           tc_fence_before();
           mbar_arrive(tdp_free);
+          if (t == 0) TR(it, 10);
         }
         if (rd > 0) {                          // staging reused: previous reduce must have read it
           if (t == 0) bulk_wait_read0();
@@ -970,6 +1014,7 @@ __global__ void __launch_bounds__(320, 1)
       if (t == 0) {
         bulk_wait_read0();
         mbar_arrive(dsbuf_free);
+        TR(it, 11);
       }
     }
     if (t == 0) bulk_wait_all0();
@@ -1036,16 +1081,26 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
     return e ? std::atoi(e) : 3;
   }();
   if (fwd_ver == 3) {
+    static const int emu = [] {
+      const char* e = std::getenv("TAWPIPE_FA_EMU");   // exponentials per 8 computed on the FMA pipe
+      return e ? std::atoi(e) : 0;
+    }();
     dim3 grid3(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+#define FWD3_LAUNCH(D, E)                                                                              \
+  do {                                                                                                 \
+    static bool once = (prep(fa_fwd3_kernel<D, E>, Fwd3Smem<D>::BYTES), true);                        \
+    (void)once;                                                                                        \
+    fa_fwd3_kernel<D, E><<<grid3, 192, Fwd3Smem<D>::BYTES, s>>>(tm, o, lse, S, nh, scale2);           \
+  } while (0)
     if (dh == 128) {
-      static bool once = (prep(fa_fwd3_kernel<128>, Fwd3Smem<128>::BYTES), true);
-      (void)once;
-      fa_fwd3_kernel<128><<<grid3, 192, Fwd3Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+      if (emu == 2) FWD3_LAUNCH(128, 2);
+      else if (emu == 3) FWD3_LAUNCH(128, 3);
+      else if (emu == 4) FWD3_LAUNCH(128, 4);
+      else FWD3_LAUNCH(128, 0);
     } else {
-      static bool once = (prep(fa_fwd3_kernel<64>, Fwd3Smem<64>::BYTES), true);
-      (void)once;
-      fa_fwd3_kernel<64><<<grid3, 192, Fwd3Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+      FWD3_LAUNCH(64, 0);
     }
+#undef FWD3_LAUNCH
     TP_CUDA(cudaGetLastError());
     g_kstats.launches++;
     return;
@@ -1094,16 +1149,24 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   const float scale = 1.0f / sqrtf(static_cast<float>(dh));
   const float scale2 = LOG2E * scale;
   dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+  static unsigned long long* trace = [] {
+    unsigned long long* p = nullptr;
+    if (std::getenv("TAWPIPE_FA_TRACE")) {
+      cudaMalloc(&p, 32 * 16 * 8);
+      cudaMemset(p, 0, 32 * 16 * 8);
+    }
+    return p;
+  }();
   if (dh == 128) {
     static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
     (void)once;
     fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse, delta, dq_acc, dqkv, S, nh, scale,
-                                                               scale2);
+                                                               scale2, trace);
   } else {
     static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
     (void)once;
     fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse, delta, dq_acc, dqkv, S, nh, scale,
-                                                             scale2);
+                                                             scale2, trace);
   }
   {
     cudaError_t e = cudaGetLastError();
@@ -1119,6 +1182,19 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
     }
   }
   fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
+  if (trace) {
+    unsigned long long h[32 * 16];
+    TP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
+    static const char* names[12] = {"mma:S_issued", "mma:tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
+                                    "cmp:p_done", "cmp:dp_full", "cmp:dsbuf_ok", "cmp:ds_done", "dq:mm2_done",
+                                    "dq:tdp_free", "dq:dsbuf_free"};
+    const unsigned long long t0 = h[0];
+    for (int it = 0; it < 12; ++it) {
+      std::fprintf(stderr, "it %2d:", it);
+      for (int e = 0; e < 12; ++e) std::fprintf(stderr, " %s=%lld", names[e], (long long)(h[it * 16 + e] - t0));
+      std::fprintf(stderr, "\n");
+    }
+  }
   TP_CUDA(cudaGetLastError());
   g_kstats.launches += 3;
 }

@@ -1,6 +1,6 @@
 #!/bin/bash
 # full ncu capture of the attention kernels (one launch each) at the C3 shape
 python tools/attn_big.py 32768 32 > gpurun_out/plain_attn.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"fa_(bwd|fwd2)_kernel" -s 2 -c 2 -o gpurun_out/prof_attn2 \
-    python tools/attn_big.py 32768 32 > gpurun_out/ncu_attn2.log 2>&1
-echo "rc=$?"; tail -3 gpurun_out/ncu_attn2.log
+ncu --set full --clock-control none --import-source on -k regex:"fa_(bwd|fwd3)_kernel" -s 2 -c 2 -o gpurun_out/prof_attn3 \
+    python tools/attn_big.py 32768 32 > gpurun_out/ncu_attn3.log 2>&1
+echo "rc=$?"; tail -2 gpurun_out/ncu_attn3.log

@@ -293,6 +293,47 @@ __global__ void adamw_kernel(Contribs c, int n_contrib, int own_k, int own_f32, 
   }
 }
 
+// 4 elements per thread, 16-byte accesses to master/m/v (n % 4 == 0, 16-byte aligned stripes)
+template <typename W>
+__global__ void adamw_v4_kernel(Contribs c, int n_contrib, int own_k, int own_f32, float* __restrict__ master,
+                                float* __restrict__ m, float* __restrict__ v, W* __restrict__ wire, int64_t n,
+                                int64_t unit_off, int64_t nd0_lo, int64_t nd0_hi, int64_t nd1_lo, int64_t nd1_hi,
+                                AdamParams hp) {
+  const int64_t n4 = n / 4;
+  for (int64_t i4 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i4 < n4;
+       i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = i4 * 4;
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = 0; k < n_contrib; ++k) {  // ascending group index (R16)
+      if (k == own_k && own_f32) {
+        const float4 x = reinterpret_cast<const float4*>(c.p[k])[i4];
+        g[0] += x.x; g[1] += x.y; g[2] += x.z; g[3] += x.w;
+      } else {
+        const W* src = static_cast<const W*>(c.p[k]) + i;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) g[e] += to_f(src[e]);
+      }
+    }
+    float4 th4 = reinterpret_cast<float4*>(master)[i4];
+    float4 m4 = reinterpret_cast<float4*>(m)[i4];
+    float4 v4 = reinterpret_cast<float4*>(v)[i4];
+    float th[4] = {th4.x, th4.y, th4.z, th4.w}, mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t pos = unit_off + i + e;
+      const bool decay = !((pos >= nd0_lo && pos < nd0_hi) || (pos >= nd1_lo && pos < nd1_hi));
+      if (decay) th[e] *= 1.f - hp.lr * hp.wd;
+      mm[e] = hp.beta1 * mm[e] + (1.f - hp.beta1) * g[e];
+      vv[e] = hp.beta2 * vv[e] + (1.f - hp.beta2) * g[e] * g[e];
+      th[e] -= hp.lr * (mm[e] / hp.bc1) / (sqrtf(vv[e] / hp.bc2) + hp.eps);
+      wire[i + e] = from_f<W>(th[e]);
+    }
+    reinterpret_cast<float4*>(master)[i4] = make_float4(th[0], th[1], th[2], th[3]);
+    reinterpret_cast<float4*>(m)[i4] = make_float4(mm[0], mm[1], mm[2], mm[3]);
+    reinterpret_cast<float4*>(v)[i4] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+  }
+}
+
 // ------------------------------------------------------------------------------------ bf16 vectorised variants
 // 16-byte accesses (8 bf16 per thread), no 64-bit index division in the inner loop.
 __device__ __forceinline__ void ld8(const bf16* p, float (&f)[8]) {
@@ -404,54 +445,61 @@ __global__ void rmsnorm_fwd_v8_kernel(const bf16* __restrict__ x, const bf16* __
   }
 }
 
-// one warp per row (RW rows per warp for the dγ partial sums, then one atomicAdd per column per warp)
-template <int NV, int RW>
-__global__ void rmsnorm_bwd_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                      const bf16* __restrict__ g, const float* __restrict__ rstd,
-                                      const bf16* __restrict__ res, bf16* __restrict__ dx, float* __restrict__ dg_acc,
-                                      int64_t rows, int H) {
-  const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
+// dx only: one warp per row (dγ is a separate column reduction below)
+template <int NV>
+__global__ void rmsnorm_bwd_dx_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                         const bf16* __restrict__ g, const float* __restrict__ rstd,
+                                         const bf16* __restrict__ res, bf16* __restrict__ dx, int64_t rows, int H) {
+  const int64_t row = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  float dg[NV][8];
-  float gv[NV][8];
+  if (row >= rows) return;
+  const float r = rstd[row];
+  float d[NV][8], xv[NV][8], gv[NV][8];
+  float dot = 0.f;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
+    ld8(dy + row * H + (i * 32 + lane) * 8, d[i]);
+    ld8(x + row * H + (i * 32 + lane) * 8, xv[i]);
     ld8(g + (i * 32 + lane) * 8, gv[i]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) dg[i][k] = 0.f;
+    for (int k = 0; k < 8; ++k) dot += d[i][k] * gv[i][k] * xv[i][k];
   }
-  for (int rr = 0; rr < RW; ++rr) {
-    const int64_t row = w * RW + rr;
-    if (row >= rows) break;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  const float coef = r * r * r * dot / H;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float o8[8], rs[8];
+    if (res) ld8(res + row * H + (i * 32 + lane) * 8, rs);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o8[k] = r * d[i][k] * gv[i][k] - xv[i][k] * coef + (res ? rs[k] : 0.f);
+    st8(dx + row * H + (i * 32 + lane) * 8, o8);
+  }
+}
+
+// dγ_c += Σ_rows dy_rc · x_rc · r_r : block = 8 warps over a 256-column block and a 256-row chunk
+__global__ void rmsnorm_dgamma_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
+                                         const float* __restrict__ rstd, float* __restrict__ dg_acc, int64_t rows,
+                                         int H) {
+  __shared__ float part[8][256];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c0 = blockIdx.x * 256 + lane * 8;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 256;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int64_t row = r0 + w; row < r0 + 256 && row < rows; row += 8) {
+    float d[8], xv[8];
+    ld8(dy + row * H + c0, d);
+    ld8(x + row * H + c0, xv);
     const float r = rstd[row];
-    float d[NV][8], xv[NV][8];
-    float dot = 0.f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      ld8(dy + row * H + (i * 32 + lane) * 8, d[i]);
-      ld8(x + row * H + (i * 32 + lane) * 8, xv[i]);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        dot += d[i][k] * gv[i][k] * xv[i][k];
-        dg[i][k] += d[i][k] * xv[i][k] * r;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const float coef = r * r * r * dot / H;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      float o8[8], rs[8];
-      if (res) ld8(res + row * H + (i * 32 + lane) * 8, rs);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) o8[k] = r * d[i][k] * gv[i][k] - xv[i][k] * coef + (res ? rs[k] : 0.f);
-      st8(dx + row * H + (i * 32 + lane) * 8, o8);
-    }
+    for (int k = 0; k < 8; ++k) acc[k] += d[k] * xv[k] * r;
   }
 #pragma unroll
-  for (int i = 0; i < NV; ++i)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) atomicAdd(&dg_acc[(i * 32 + lane) * 8 + k], dg[i][k]);
+  for (int k = 0; k < 8; ++k) part[w][lane * 8 + k] = acc[k];
+  __syncthreads();
+  const float v = part[0][threadIdx.x] + part[1][threadIdx.x] + part[2][threadIdx.x] + part[3][threadIdx.x] +
+                  part[4][threadIdx.x] + part[5][threadIdx.x] + part[6][threadIdx.x] + part[7][threadIdx.x];
+  atomicAdd(&dg_acc[blockIdx.x * 256 + threadIdx.x], v);
 }
 
 inline unsigned grid_stride_blocks(int64_t n) {
@@ -497,15 +545,20 @@ template <typename T>
 void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
                  int64_t rows, int H, cudaStream_t s) {
   if constexpr (std::is_same<T, bf16>::value) {
-    constexpr int RW = 16;  // rows per warp
-    const unsigned blocks = static_cast<unsigned>((rows + 8 * RW - 1) / (8 * RW));
-    switch (H) {
-      case 256: rmsnorm_bwd_v8_kernel<1, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
-      case 1024: rmsnorm_bwd_v8_kernel<4, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
-      case 2048: rmsnorm_bwd_v8_kernel<8, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
-      case 4096: rmsnorm_bwd_v8_kernel<16, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
-      case 5120: rmsnorm_bwd_v8_kernel<20, RW><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H); LAUNCHED(); return;
-      default: break;
+    if (H % 256 == 0 && (H == 256 || H == 1024 || H == 2048 || H == 4096 || H == 5120)) {
+      const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
+      switch (H) {
+        case 256: rmsnorm_bwd_dx_v8_kernel<1><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
+        case 1024: rmsnorm_bwd_dx_v8_kernel<4><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
+        case 2048: rmsnorm_bwd_dx_v8_kernel<8><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
+        case 4096: rmsnorm_bwd_dx_v8_kernel<16><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
+        default: rmsnorm_bwd_dx_v8_kernel<20><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
+      }
+      LAUNCHED();
+      rmsnorm_dgamma_v8_kernel<<<dim3(H / 256, static_cast<unsigned>((rows + 255) / 256)), 256, 0, s>>>(
+          dy, x, rstd, dg_acc, rows, H);
+      LAUNCHED();
+      return;
     }
   }
   constexpr int RB = 32;
@@ -597,8 +650,12 @@ void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_
   for (int k = 0; k < n_contrib; ++k) c.p[k] = contrib[k];
   const int64_t l0 = n_nd > 0 ? nd_lo[0] : 0, h0 = n_nd > 0 ? nd_hi[0] : 0;
   const int64_t l1 = n_nd > 1 ? nd_lo[1] : 0, h1 = n_nd > 1 ? nd_hi[1] : 0;
-  adamw_kernel<W><<<grid_stride_blocks(n), 256, 0, s>>>(c, n_contrib, own_k, own_f32 ? 1 : 0, master, m, v, wire, n,
-                                                        unit_off, l0, h0, l1, h1, p);
+  if (n % 4 == 0)
+    adamw_v4_kernel<W><<<grid_stride_blocks(n / 4), 256, 0, s>>>(c, n_contrib, own_k, own_f32 ? 1 : 0, master, m, v,
+                                                                 wire, n, unit_off, l0, h0, l1, h1, p);
+  else
+    adamw_kernel<W><<<grid_stride_blocks(n), 256, 0, s>>>(c, n_contrib, own_k, own_f32 ? 1 : 0, master, m, v, wire, n,
+                                                          unit_off, l0, h0, l1, h1, p);
   LAUNCHED();
 }
 

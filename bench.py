@@ -290,6 +290,35 @@ def run_ours(args, c):
         "ledger_elems": ledger,
         "alloc_gb": st["alloc_gb"],
     }
+    sess.close()
+    # in-library comparison schedules, same workload (north_star: WeiPipe-style ring and FSDP-style global)
+    if world > 1 and not args.no_baselines:
+        out["baselines"] = {}
+        for name, Gb, sched in (("fsdp_global_D1", world, T.GWPS), ("weipipe_ring", 1, T.RING)):
+            T.bootstrap(rank, world, local, pg_backend="gloo")
+            db = T.ModelDims(**{**dims.__dict__, "schedule": sched})
+            sb = T.Session(world, Gb, db, N)
+            sb.set_timing(True)
+            for i in range(max(1, min(args.warmup, 2))):
+                sb.step_device(tok_dev[i % 2].data_ptr())
+            barrier()
+            torch.cuda.synchronize()
+            nb = max(1, min(args.steps, 2))
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record()
+            sts = []
+            for i in range(nb):
+                sb.step_device(tok_dev[i % 2].data_ptr())
+                sts.append(sb.stats())
+            b1.record()
+            torch.cuda.synchronize()
+            barrier()
+            bms = max_over_ranks(b0.elapsed_time(b1) / nb)
+            bexp = max_over_ranks(statistics.mean(x["exposed_comm_ms"] for x in sts))
+            out["baselines"][name] = {"value": tokens_step / (bms / 1e3), "unit": "tokens/s", "ms_per_step": bms,
+                                      "exposed_comm_ms": bexp, "group_size": Gb, "steps": nb,
+                                      "ledger_elems": sb.ledger()}
+            sb.close()
     if rank == 0:
         if not args.no_cpu_baseline:
             try:
@@ -297,7 +326,6 @@ def run_ours(args, c):
             except Exception as e:
                 out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
         print(json.dumps(out), flush=True)
-    sess.close()
 
 
 def main():
@@ -309,6 +337,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cco", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-baselines", action="store_true", help="skip the in-library FSDP / ring comparison runs")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":

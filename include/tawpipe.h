@@ -44,6 +44,11 @@ extern "C" {
 /* schedule flags (tawpipe_dims.schedule) */
 #define TAWPIPE_GWPS   0        /* default: the paper's schedule                                     */
 #define TAWPIPE_NO_CCO 1        /* ablation: gather of layer l+1 waits for compute of l */
+#define TAWPIPE_RING   2        /* WeiPipe-style ring (also the paper's "w/o GWPS"
+                                   ablation): whole layers owned by device l mod P (needs
+                                   group_size 1); weights hop owner -> owner+1 -> ... around the ring,
+                                   gradients accumulate hop by hop from owner+1 and end at the owner.
+                                   The FSDP-style global schedule is group_size = n_devices (D = 1).     */
 
 #define TAWPIPE_LEDGER_N 24     /* see tawpipe_ledger */
 #define TAWPIPE_STATS_N  16     /* see tawpipe_stats  */
@@ -59,7 +64,7 @@ typedef struct tawpipe_dims {
   int32_t micro_bs;      /* B, sequences per micro-batch                                          */
   int32_t dtype;         /* TAWPIPE_FP32 | TAWPIPE_BF16                                          */
   int32_t ckpt;          /* 1: keep only each layer's input h_l, recompute in backward */
-  int32_t schedule;      /* TAWPIPE_GWPS | TAWPIPE_NO_CCO                                        */
+  int32_t schedule;      /* TAWPIPE_GWPS or TAWPIPE_RING, optionally | TAWPIPE_NO_CCO              */
   int32_t reserved;      /* must be 0                                                            */
   float lr, beta1, beta2, adam_eps, weight_decay;   /* AdamW, torch semantics (R1)               */
   float rms_eps, rope_theta;                        /* 1e-5, 10000 (R10)                          */

@@ -78,3 +78,42 @@ def closed_form(L: int, P: int, G: int, k: int, s: int, e: int, f: int, r: int =
 def block_received(ledger: list) -> int:
     """Total decoder-block elements received (weights + grads, intra + inter)."""
     return sum(ledger[index(kd, c, "recv", "block")] for kd in KINDS for c in CLASSES)
+
+
+def ring_ledger(L: int, P: int, d: int, s: int, e: int, f: int, r: int = 1) -> list:
+    """WeiPipe-style ring schedule, written from its definition:
+    whole units, unit u owned by device o(u) (layer l: l mod P; E: 0; F: P−1); a weight gather moves u
+    o → o+1 → … → o−1 (each device except o receives it once, each device except o−1 forwards it once); a
+    gradient reduction moves the running partial o+1 → … → o (each device except o+1 receives one partial,
+    each device except o sends one).  Same step sequence as the GWPS schedule (r = 1 reuses layer L−1)."""
+    out = [0] * N_COUNTERS
+    if P == 1:
+        return out
+    units = [("block", l % P, s) for l in range(L)]
+    E, F = ("E", 0, e), ("F", P - 1, f)
+
+    def gather(u):
+        cls, o, n = u
+        if d != o:
+            out[index("w", "inter", "recv", cls)] += n
+        if (d + 1) % P != o:
+            out[index("w", "inter", "sent", cls)] += n
+
+    def reduce(u):
+        cls, o, n = u
+        if d != (o + 1) % P:
+            out[index("g", "inter", "recv", cls)] += n
+        if d != o:
+            out[index("g", "inter", "sent", cls)] += n
+
+    gather(E)
+    for u in units:
+        gather(u)
+    gather(F)
+    reduce(F)
+    for l in range(L - 1, -1, -1):
+        if not (r == 1 and l == L - 1):
+            gather(units[l])
+        reduce(units[l])
+    reduce(E)
+    return out

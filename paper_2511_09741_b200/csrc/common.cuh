@@ -107,6 +107,9 @@ template <typename T>
 void cast_f32(const float* x, T* y, int64_t n, cudaStream_t s);
 template <typename T>
 void cast_to_f32(const T* x, float* y, int64_t n, cudaStream_t s);
+// y = (T)(a + b) with a in T and b fp32 (one hop of the ring gradient reduction)
+template <typename T>
+void add_cast(const T* a, const float* b, T* y, int64_t n, cudaStream_t s);
 template <typename T>
 void init_normal(T* wire, float* master, int64_t n, int64_t global_off, uint64_t seed, float std, cudaStream_t s);
 void fill_f32(float* x, int64_t n, float v, cudaStream_t s);

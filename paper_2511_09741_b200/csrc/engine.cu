@@ -71,6 +71,7 @@ struct Ctx {
   int H = 0, nh = 0, dh = 0, I = 0, V = 0, S = 0, Bm = 1;
   int64_t T = 0, phi = 0;
   bool bf = false;
+  bool ring = false;  // TAWPIPE_RING schedule
   size_t esz = 4;
   ncclComm_t wg = nullptr, wr = nullptr, gg = nullptr, gr = nullptr;
   cudaStream_t cs = nullptr, ws = nullptr, gs = nullptr;
@@ -270,6 +271,18 @@ void ledger_gather(const Unit& u, int G, int D, uint64_t* led) {
     led[ledger_index(K_W, C_INTRA, D_SENT, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
   }
 }
+// WeiPipe-style ring (G = 1): device d receives layer u from d-1 unless it owns it and forwards it to d+1
+// unless d+1 owns it; the gradient partial starts at owner+1 and ends at the owner (one P2P per hop).
+void ledger_gather_ring(const Unit& u, int d, int P, uint64_t* led) {
+  if (P == 1) return;
+  if (d != u.owner) led[ledger_index(K_W, C_INTER, D_RECV, u.cls)] += static_cast<uint64_t>(u.s);
+  if ((d + 1) % P != u.owner) led[ledger_index(K_W, C_INTER, D_SENT, u.cls)] += static_cast<uint64_t>(u.s);
+}
+void ledger_reduce_ring(const Unit& u, int d, int P, uint64_t* led) {
+  if (P == 1) return;
+  if (d != (u.owner + 1) % P) led[ledger_index(K_G, C_INTER, D_RECV, u.cls)] += static_cast<uint64_t>(u.s);
+  if (d != u.owner) led[ledger_index(K_G, C_INTER, D_SENT, u.cls)] += static_cast<uint64_t>(u.s);
+}
 void ledger_reduce(const Unit& u, int G, int D, uint64_t* led) {
   if (G > 1) {
     led[ledger_index(K_G, C_INTRA, D_RECV, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
@@ -298,6 +311,14 @@ void gather(int uid, void* dst) {
   if (g->P == 1) return;  // nothing to move; the compute reads the owned copy in place
   Timed t(g->ws, 5, 0);
   void* own = wptr(g->wire, u.off);
+  if (g->ring) {  // owner -> owner+1 -> ... : receive from d-1, then forward to d+1 (stream-ordered)
+    const int d = g->rank, P = g->P;
+    void* buf = u.owned ? own : dst;
+    if (!u.owned) TP_NCCL(ncclRecv(buf, u.n_pad, wire_type(), (d + P - 1) % P, g->wr, g->ws));
+    if ((d + 1) % P != u.owner) TP_NCCL(ncclSend(buf, u.n_pad, wire_type(), (d + 1) % P, g->wr, g->ws));
+    ledger_gather_ring(u, d, P, g->ledger);
+    return;
+  }
   if (g->D > 1) {
     TP_NCCL(ncclGroupStart());
     if (u.owned) {
@@ -316,8 +337,48 @@ void gather(int uid, void* dst) {
 }
 
 // a8 + a9: reduce-scatter in the group, rail P2P to the owner, ascending-k accumulate + AdamW, on gs
+void adam_update(const Unit& u, const void* const* contrib, int n_contrib, int own_k, bool own_f32);
+
+// WeiPipe-style ring reduction: owner+1 starts the partial sum, each device adds its local fp32 gradient and
+// forwards it (wire dtype), the owner adds its own and applies AdamW
+void reduce_ring(const Unit& u, float* gacc) {
+  cudaStream_t s = g->gs;
+  const int d = g->rank, P = g->P;
+  if (P == 1) {
+    const void* c0 = gacc;
+    adam_update(u, &c0, 1, 0, true);
+    return;
+  }
+  const int prev = (d + P - 1) % P, next = (d + 1) % P;
+  const bool first = (d == (u.owner + 1) % P);
+  if (!first) {
+    Timed t(s, 6, 0);
+    TP_NCCL(ncclRecv(g->crecv, u.n_pad, wire_type(), prev, g->gr, s));
+  }
+  if (u.owned) {
+    const void* contrib[2] = {gacc, g->crecv};
+    adam_update(u, contrib, 2, 0, true);
+  } else {
+    {
+      Timed t(s, 4, 0);
+      if (first)
+        BY_TYPE(cast_f32<float>(gacc, (float*)g->gwire, u.n_pad, s), cast_f32<bf16>(gacc, (bf16*)g->gwire, u.n_pad, s));
+      else
+        BY_TYPE(add_cast<float>((const float*)g->crecv, gacc, (float*)g->gwire, u.n_pad, s),
+                add_cast<bf16>((const bf16*)g->crecv, gacc, (bf16*)g->gwire, u.n_pad, s));
+    }
+    Timed t(s, 6, 0);
+    TP_NCCL(ncclSend(g->gwire, u.n_pad, wire_type(), next, g->gr, s));
+  }
+  ledger_reduce_ring(u, d, P, g->ledger);
+}
+
 void reduce_and_update(int uid, float* gacc) {
   const Unit& u = g->units[uid];
+  if (g->ring) {
+    reduce_ring(u, gacc);
+    return;
+  }
   cudaStream_t s = g->gs;
   const void* own_partial = gacc;
   bool own_f32 = true;
@@ -349,6 +410,12 @@ void reduce_and_update(int uid, float* gacc) {
   const void* contrib[8];
   int idx = 0;
   for (int kk = 0; kk < g->D; ++kk) contrib[kk] = (kk == g->k) ? own_partial : wptr(g->crecv, (idx++) * u.s);
+  adam_update(u, contrib, g->D, g->k, own_f32);
+}
+
+// a9: fused accumulate of the group contributions (ascending order) + AdamW on this rank's owned stripe, on gs
+void adam_update(const Unit& u, const void* const* contrib, int n_contrib, int own_k, bool own_f32) {
+  cudaStream_t s = g->gs;
   AdamParams hp;
   hp.lr = g->dims.lr;
   hp.beta1 = g->dims.beta1;
@@ -358,10 +425,10 @@ void reduce_and_update(int uid, float* gacc) {
   hp.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta1), g->step_t));
   hp.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta2), g->step_t));
   const int64_t stripe_off = static_cast<int64_t>(g->j) * u.s;
-  Timed t(s, 2, (2.0 * g->D * g->esz + 26.0) * u.s);
-  BY_TYPE(adamw_fused<float>(contrib, g->D, g->k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
+  Timed t(s, 2, (2.0 * n_contrib * g->esz + 26.0) * u.s);
+  BY_TYPE(adamw_fused<float>(contrib, n_contrib, own_k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
                              (float*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s),
-          adamw_fused<bf16>(contrib, g->D, g->k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
+          adamw_fused<bf16>(contrib, n_contrib, own_k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
                             (bf16*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s));
 }
 
@@ -656,6 +723,9 @@ void validate(int P, int G, int L, const tawpipe_dims* d, int N, int world) {
   TP_CHECK((d->hidden / d->heads) % 2 == 0, TAWPIPE_ECONFIG, "d_h must be even (rotate-half RoPE)");
   TP_CHECK(d->dtype == TAWPIPE_FP32 || d->dtype == TAWPIPE_BF16, TAWPIPE_ECONFIG, "dtype must be FP32 or BF16");
   TP_CHECK(d->reserved == 0, TAWPIPE_ECONFIG, "reserved must be 0");
+  TP_CHECK((d->schedule & ~(TAWPIPE_NO_CCO | TAWPIPE_RING)) == 0, TAWPIPE_ECONFIG, "unknown schedule flag");
+  TP_CHECK(!(d->schedule & TAWPIPE_RING) || G == 1, TAWPIPE_ECONFIG,
+           "TAWPIPE_RING owns whole layers per device: group_size must be 1");
   if (d->dtype == TAWPIPE_BF16) {
     const int dh = d->hidden / d->heads;
     TP_CHECK(dh == 64 || dh == 128, TAWPIPE_ECONFIG, "bf16 path: d_h must be 64 or 128");
@@ -737,6 +807,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   c.Bm = d->micro_bs;
   c.T = static_cast<int64_t>(c.Bm) * c.S;
   c.bf = d->dtype == TAWPIPE_BF16;
+  c.ring = (d->schedule & TAWPIPE_RING) != 0;
   c.esz = c.bf ? 2 : 4;
   const int64_t H = c.H, I = c.I, V = c.V;
   c.phi = 4 * H * H + 3 * H * I + 2 * H;
@@ -970,17 +1041,27 @@ int tawpipe_plan(int n_devices, int group_size, int n_layers, const tawpipe_dims
     const int G = group_size, D = n_devices / group_size, L = n_layers;
     Plan pl = make_plan(n_devices, G, L, dims->hidden, dims->ffn, dims->vocab, rank);
     uint64_t led[TAWPIPE_LEDGER_N] = {};
+    const bool ring = (dims->schedule & TAWPIPE_RING) != 0;
+    const int P = n_devices;
+    auto gat = [&](const Unit& u) {
+      if (ring) ledger_gather_ring(u, rank, P, led);
+      else ledger_gather(u, G, D, led);
+    };
+    auto red = [&](const Unit& u) {
+      if (ring) ledger_reduce_ring(u, rank, P, led);
+      else ledger_reduce(u, G, D, led);
+    };
     // the step's communication sequence (run_step): E gather, forward gathers 0..L-1, F gather, F reduction,
     // backward gathers L-2..0 (layer L-1 reuses its forward buffer, R12) with reductions L-1..0, E reduction
-    ledger_gather(pl.units[L], G, D, led);
-    for (int l = 0; l < L; ++l) ledger_gather(pl.units[l], G, D, led);
-    ledger_gather(pl.units[L + 1], G, D, led);
-    ledger_reduce(pl.units[L + 1], G, D, led);
+    gat(pl.units[L]);
+    for (int l = 0; l < L; ++l) gat(pl.units[l]);
+    gat(pl.units[L + 1]);
+    red(pl.units[L + 1]);
     for (int l = L - 1; l >= 0; --l) {
-      if (l != L - 1) ledger_gather(pl.units[l], G, D, led);
-      ledger_reduce(pl.units[l], G, D, led);
+      if (l != L - 1) gat(pl.units[l]);
+      red(pl.units[l]);
     }
-    ledger_reduce(pl.units[L], G, D, led);
+    red(pl.units[L]);
     if (ledger_out) std::memcpy(ledger_out, led, sizeof(led));
     if (shard_elems_out) *shard_elems_out = pl.owned_total;
   });

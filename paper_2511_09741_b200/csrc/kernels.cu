@@ -232,6 +232,12 @@ __global__ void cast_to_f32_kernel(const T* __restrict__ x, float* __restrict__ 
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     y[i] = to_f(x[i]);
 }
+template <typename T>
+__global__ void add_cast_kernel(const T* __restrict__ a, const float* __restrict__ b, T* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = from_f<T>(to_f(a[i]) + b[i]);
+}
 __global__ void fill_kernel(float* __restrict__ x, int64_t n, float v) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -632,6 +638,11 @@ void cast_to_f32(const T* x, float* y, int64_t n, cudaStream_t s) {
   cast_to_f32_kernel<T><<<grid_stride_blocks(n), 256, 0, s>>>(x, y, n);
   LAUNCHED();
 }
+template <typename T>
+void add_cast(const T* a, const float* b, T* y, int64_t n, cudaStream_t s) {
+  add_cast_kernel<T><<<grid_stride_blocks(n), 256, 0, s>>>(a, b, y, n);
+  LAUNCHED();
+}
 void fill_f32(float* x, int64_t n, float v, cudaStream_t s) {
   fill_kernel<<<grid_stride_blocks(n), 256, 0, s>>>(x, n, v);
   LAUNCHED();
@@ -670,6 +681,7 @@ void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_
   template void cross_entropy<T>(T*, const int32_t*, int64_t, int, float, float*, cudaStream_t);                 \
   template void cast_f32<T>(const float*, T*, int64_t, cudaStream_t);                                            \
   template void cast_to_f32<T>(const T*, float*, int64_t, cudaStream_t);                                         \
+  template void add_cast<T>(const T*, const float*, T*, int64_t, cudaStream_t);                                  \
   template void init_normal<T>(T*, float*, int64_t, int64_t, uint64_t, float, cudaStream_t);                     \
   template void adamw_fused<T>(const void* const*, int, int, bool, float*, float*, float*, T*, int64_t, int64_t, \
                                const int64_t*, const int64_t*, int, AdamParams, cudaStream_t);

@@ -19,16 +19,19 @@ from oracle import ledger as LG
 torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
-# (name, base dims, P, G, L, N, dtype, ckpt, no_cco)
+# (name, base dims, P, G, L, N, dtype, ckpt, no_cco, ring)
 CASES = [
-    ("c0-1x2-fsdp", C0, 2, 2, 2, 4, 0, 0, False),
-    ("c0-2x1-p2p", C0, 2, 1, 2, 4, 0, 0, False),
-    ("c0-2x2", C0, 4, 2, 2, 4, 0, 0, False),          # BASELINE.json configs[0]
-    ("c0-2x2-nocco", C0, 4, 2, 2, 4, 0, 0, True),
-    ("c0-1x4", C0, 4, 4, 2, 8, 0, 1, False),
-    ("c0-4x1", C0, 4, 1, 4, 4, 0, 0, False),
-    ("c0b-2x2-bf16", C0B, 4, 2, 2, 4, 1, 1, False),
-    ("c0b-1x2-bf16", C0B, 2, 2, 2, 2, 1, 0, False),
+    ("c0-1x2-fsdp", C0, 2, 2, 2, 4, 0, 0, False, False),
+    ("c0-2x1-p2p", C0, 2, 1, 2, 4, 0, 0, False, False),
+    ("c0-2x2", C0, 4, 2, 2, 4, 0, 0, False, False),          # BASELINE.json configs[0]
+    ("c0-2x2-nocco", C0, 4, 2, 2, 4, 0, 0, True, False),
+    ("c0-1x4", C0, 4, 4, 2, 8, 0, 1, False, False),
+    ("c0-4x1", C0, 4, 1, 4, 4, 0, 0, False, False),
+    ("c0b-2x2-bf16", C0B, 4, 2, 2, 4, 1, 1, False, False),
+    ("c0b-1x2-bf16", C0B, 2, 2, 2, 2, 1, 0, False, False),
+    ("c0-ring2", C0, 2, 1, 2, 4, 0, 0, False, True),          # NEXT-1 WeiPipe-style ring
+    ("c0-ring4", C0, 4, 1, 4, 4, 0, 1, False, True),
+    ("c0b-ring4-bf16", C0B, 4, 1, 4, 4, 1, 0, False, True),
 ]
 
 
@@ -38,8 +41,8 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco", CASES, ids=[c[0] for c in CASES])
-def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco):
+@pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco,ring", CASES, ids=[c[0] for c in CASES])
+def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco, ring):
     if not torch.cuda.is_available() or torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     cfg = oracle_cfg(base, n_layers=L)
@@ -47,7 +50,8 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--cfg", json.dumps(dict(base, n_layers=L)), "--G", str(G), "--N", str(N), "--steps", str(steps),
-           "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else [])
+           "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else []) \
+        + (["--ring"] if ring else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
@@ -72,6 +76,6 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
     H, V = cfg.hidden, cfg.vocab
     s, e, f = (OL.padded(n, G) // G for n in (om.phi(cfg), V * H, H + V * H))
     for i in range(P):
-        expect = LG.closed_form(L, P, G, i // G, s, e, f, r=1)
+        expect = LG.ring_ledger(L, P, i, s, e, f, r=1) if ring else LG.closed_form(L, P, G, i // G, s, e, f, r=1)
         for step in range(steps):
             assert [int(x) for x in res[i]["ledgers"][step]] == expect, (i, step)

@@ -93,3 +93,34 @@ def test_bootstrap_unique_id_over_gloo_world2():
     out = mgr.dict()
     mp.spawn(_uid_worker, args=(2, port, out), nprocs=2, join=True)
     assert len(out) == 2 and out[0] == out[1] and len(bytes.fromhex(out[0])) == 128
+
+
+@pytest.mark.parametrize("P,L", [(2, 2), (3, 3), (4, 4), (4, 8), (8, 8), (8, 32), (6, 6)])
+def test_ring_plan_ledger_and_3L_identity(T, P, L):
+    """NEXT-1 WeiPipe-style ring: plan ledger == the ring's definition; 3L(P−1)φ/P per device at r = 0."""
+    cfg = oracle_cfg(C0, n_layers=L)
+    H, V = cfg.hidden, cfg.vocab
+    s = OL.padded(om.phi(cfg), 1)
+    e = OL.padded(V * H, 1)
+    f = OL.padded(H + V * H, 1)
+    d = dims_for(T, cfg)
+    d.schedule = T.RING
+    for rank in range(P):
+        led, _ = T.plan(P, 1, d, P, rank)
+        assert led == LG.ring_ledger(L, P, rank, s, e, f, r=1)
+        r0 = LG.ring_ledger(L, P, rank, s, e, f, r=0)
+        assert LG.block_received(r0) * P == 3 * L * (P - 1) * s
+    # same per-device block receive total as GWPS at r = 0 (SURVEY R14: TawPipe, FSDP and a ring alike)
+    sg = OL.padded(om.phi(cfg), 1)
+    for rank in range(P):
+        gw = LG.closed_form(L, P, 1, rank, sg, e, f, r=0)
+        assert LG.block_received(gw) == LG.block_received(LG.ring_ledger(L, P, rank, s, e, f, r=0))
+
+
+def test_ring_requires_group_size_1(T):
+    cfg = oracle_cfg(C0)
+    d = dims_for(T, cfg)
+    d.schedule = T.RING
+    with pytest.raises(T.TawpipeError) as ei:
+        T.plan(4, 2, d, 4, 0)
+    assert "group_size" in str(ei.value)

@@ -14,6 +14,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -734,18 +735,21 @@ __global__ void __launch_bounds__(192, 1)
 //   warps 0-3  softmax-gradient warps, thread t <-> key row t of the tile (TMEM lane t):
 //              Pᵀ = exp2(Sᵀ·c·log2e − LSE·log2e) is written back into TMEM as packed bf16 over Sᵀ's columns
 //              (the A operand of dV += Pᵀ·dO), dSᵀ = Pᵀ⊙(dPᵀ − δ) goes to smem (A of dK, MN-major A of dQ)
-//   warps 4-7  dQ warps: read dQ_i (TMEM lanes = query rows), stage it (fp32, 128-byte swizzle) in the dSᵀ
-//              buffer once the MMAs have consumed dSᵀ, and add it into the fp32 accumulator with TMA
-//              tensor reduce-add (cp.reduce.async.bulk.tensor)
-//   warp 8     TMA producer (K, V once; Q_i, dO_i, LSE_i, δ_i double-buffered)
-//   warp 9     MMA issuer: Sᵀ, dPᵀ, dV += Pᵀ·dO, dK += dSᵀ·Q, dQ_i = dS·K (into dPᵀ's TMEM columns)
+//   warps 4-7  dQ warps: read dQ_i (TMEM lanes = query rows) into registers, stage it (fp32, 128-byte
+//              swizzle) in a dedicated smem buffer and add it into the fp32 accumulator with TMA tensor
+//              reduce-add (cp.reduce.async.bulk.tensor) -- the L2 reduction runs off the critical path
+//   warp 8     TMA producer: K, V once; Q_i (+ LSE_i, δ_i by bulk copy) double-buffered; dO_i single-buffered
+//              (released as soon as dV += Pᵀ·dO has consumed it)
+//   warp 9     MMA issuer: Sᵀ, dPᵀ, dV, dK, dQ_i (into dPᵀ's TMEM columns)
+//   TMEM: Sᵀ/Pᵀ [0,128) dPᵀ/dQ [128,256) dV [256,256+d) dK [256+d,256+2d)
 template <int DH>
 struct BwdSmem {
   static constexpr int QB = DH / 64 * ATOM;
-  static constexpr int OFF_K = 0, OFF_V = QB, OFF_Q = 2 * QB, OFF_DO = 4 * QB;  // Q, dO: 2 stages each
-  static constexpr int OFF_DS = 6 * QB;              // dSᵀ [kv][q], 2 atoms; then dQ staging (2 × 16 KB fp32)
-  static constexpr int OFF_LSE = OFF_DS + 2 * ATOM;  // 2 × 128 floats
-  static constexpr int OFF_DEL = OFF_LSE + 1024;     // 2 × 128 floats
+  static constexpr int OFF_K = 0, OFF_V = QB, OFF_Q = 2 * QB, OFF_DO = 4 * QB;  // Q: 2 stages, dO: 1
+  static constexpr int OFF_DS = 5 * QB;              // dSᵀ [kv][q], 2 atoms
+  static constexpr int OFF_STG = OFF_DS + 2 * ATOM;  // dQ staging: 2 × (128 rows × 32 fp32) per round
+  static constexpr int OFF_LSE = OFF_STG + 2 * ATOM; // 2 stages × 128 floats
+  static constexpr int OFF_DEL = OFF_LSE + 1024;     // 2 stages × 128 floats
   static constexpr int OFF_BAR = OFF_DEL + 1024;
   static constexpr int BYTES = OFF_BAR + 256;
 };
@@ -756,22 +760,21 @@ __device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 
 template <int DH>
 __global__ void __launch_bounds__(320, 1)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
-                  const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
-                  bf16* __restrict__ dqkv, int S, int nh, float scale, float scale2,
-                  unsigned long long* __restrict__ trace) {
+                  const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse,
+                  const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
+                  float scale, float scale2, unsigned long long* __restrict__ trace) {
   using L = BwdSmem<DH>;
   // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
   auto TR = [&](int it, int ev) {
-    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32)
-      trace[it * 16 + ev] = clock64();
+    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32) trace[it * 16 + ev] = clock64();
   };
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *s_full = bar + 5, *dp_full = bar + 6,
-           *tdp_free = bar + 7, *p_ready = bar + 8, *ds_ready = bar + 9, *mm2_done = bar + 10,
-           *dsbuf_free = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *do_full = bar + 5, *do_empty = bar + 6,
+           *s_full = bar + 7, *dp_full = bar + 8, *tdp_free = bar + 9, *p_ready = bar + 10, *ds_ready = bar + 11,
+           *mm2_done = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
   float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
   float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
 
@@ -789,18 +792,20 @@ __global__ void __launch_bounds__(320, 1)
     if (smem_u32(sm) & 1023) __trap();  // SW128 tiles need a 1024-byte aligned base
     tma_prefetch(&tm);
     tma_prefetch(&tmdo);
+    tma_prefetch(&tmdq);
     mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
     mbar_init(tdp_free, 128);
     mbar_init(p_ready, 128);
     mbar_init(ds_ready, 128);
     mbar_init(mm2_done, 1);
-    mbar_init(dsbuf_free, 1);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -820,14 +825,16 @@ __global__ void __launch_bounds__(320, 1)
       for (int it = 0; it < n_it; ++it) {
         const int i = jt + it, st = it & 1;
         mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * L::QB + 1024);
-        for (int a = 0; a < DH / 64; ++a) {
+        mbar_expect_tx(&q_full[st], L::QB + 1024);
+        for (int a = 0; a < DH / 64; ++a)
           tma_load_2d(sm + L::OFF_Q + st * L::QB + a * ATOM, &tm, &q_full[st], h * DH + a * 64, row0 + i * BQ);
-          tma_load_2d(sm + L::OFF_DO + st * L::QB + a * ATOM, &tmdo, &q_full[st], h * DH + a * 64, row0 + i * BQ);
-        }
         const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ;
         bulk_load(lse_s + st * 128, lse + li, 512, &q_full[st]);
         bulk_load(del_s + st * 128, delta + li, 512, &q_full[st]);
+        mbar_wait(do_empty, (it & 1) ^ 1);
+        mbar_expect_tx(do_full, L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, do_full, h * DH + a * 64, row0 + i * BQ);
       }
     }
   } else if (warp == 9) {
@@ -835,18 +842,24 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
       constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
       constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
-      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS);
-      mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_it; ++it) {
+      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS),
+                     sDO = smem_u32(sm + L::OFF_DO);
+      auto issue_s = [&](int it) {  // Sᵀ_it = K·Q_itᵀ into tS
         const int st = it & 1;
-        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB), sDO = smem_u32(sm + L::OFF_DO + st * L::QB);
         mbar_wait(&q_full[st], (it >> 1) & 1);
         tc_fence_after();
-        // tS held Pᵀ_{it-1}, read by the softmax warps before ds_ready(it-1), which was awaited below
+        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
         umma_commit(s_full);
         TR(it, 0);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
+        mbar_wait(do_full, it & 1);
         if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
         TR(it, 1);
         tc_fence_after();
@@ -858,8 +871,12 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
+        umma_commit(do_empty);
         mbar_wait(ds_ready, it & 1);
         TR(it, 3);
+        // Pᵀ_it fully consumed (dV issued before, dS pass done): Sᵀ_{it+1} goes first so that the softmax warps
+        // compute Pᵀ_{it+1} while dK_it and dQ_it run on the tensor core
+        if (it + 1 < n_it) issue_s(it + 1);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
@@ -874,41 +891,51 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     uint8_t* sDS = sm + L::OFF_DS;
     for (int it = 0; it < n_it; ++it) {
-      const float* ls = lse_s + (it & 1) * 128;   // filled by the producer with Q_i (q_full[it & 1])
-      const float* dl = del_s + (it & 1) * 128;
+      const int st = it & 1;
+      const float* ls = lse_s + st * 128;
+      const float* dl = del_s + st * 128;
+      mbar_wait(&q_full[st], (it >> 1) & 1);   // LSE_i, δ_i landed (bulk copies on the same barrier as Q_i)
       mbar_wait(s_full, it & 1);
       if (t == 0) TR(it, 4);
       tc_fence_after();
 #pragma unroll
-      for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
-        uint32_t uu[2][32];
-        tmem_ld32(tS + lane_off + cp * 32, uu[0]);
-        tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
-        tmem_wait_ld();
+      // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
+      auto p_pass = [&](auto diag) {
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c = cp + h2;
-          uint32_t pw[16];
+        for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+          uint32_t uu[2][32];
+          tmem_ld32(tS + lane_off + cp * 32, uu[0]);
+          tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
+          tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            float p0 = ex2_mix(fmaf(__uint_as_float(uu[h2][k]), scale2, -ls[c * 32 + k] * LOG2E), k);
-            float p1 = ex2_mix(fmaf(__uint_as_float(uu[h2][k + 1]), scale2, -ls[c * 32 + k + 1] * LOG2E), k + 1);
-            if (it == 0) {  // diagonal tile: query index < key index is masked
-              if (c * 32 + k < t) p0 = 0.f;
-              if (c * 32 + k + 1 < t) p1 = 0.f;
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int c = cp + h2;
+            uint32_t pw[16];
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              float p0 = ex2(fmaf(__uint_as_float(uu[h2][k]), scale2, -ls[c * 32 + k]));
+              float p1 = ex2(fmaf(__uint_as_float(uu[h2][k + 1]), scale2, -ls[c * 32 + k + 1]));
+              if (decltype(diag)::value) {  // query index < key index is masked
+                if (c * 32 + k < t) p0 = 0.f;
+                if (c * 32 + k + 1 < t) p1 = 0.f;
+              }
+              pw[k / 2] = pack_bf16(p0, p1);
             }
-            pw[k / 2] = pack_bf16(p0, p1);
+            tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < cp*32+64)
           }
-          tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < cp*32+64)
         }
-      }
+      };
+      if (it == 0)
+        p_pass(std::true_type{});
+      else
+        p_pass(std::false_type{});
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_ready);
       if (t == 0) TR(it, 5);
       mbar_wait(dp_full, it & 1);
       if (t == 0) TR(it, 6);
-      if (it > 0) mbar_wait(dsbuf_free, (it - 1) & 1);  // dSᵀ buffer: MMAs and the dQ staging of it-1 done
+      if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ of the previous tile consumed by dK / dQ
       if (t == 0) TR(it, 7);
       tc_fence_after();
 #pragma unroll
@@ -975,34 +1002,30 @@ __global__ void __launch_bounds__(320, 1)
     const int q = warp & 3;
     const int t = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sm + L::OFF_DS;
+    uint8_t* stg = sm + L::OFF_STG;
     for (int it = 0; it < n_it; ++it) {
       const int i = jt + it;
-      mbar_wait(mm2_done, it & 1);   // dQ_i complete; dSᵀ consumed by the MMAs
+      mbar_wait(mm2_done, it & 1);   // dQ_i complete
       if (t == 0) TR(it, 9);
       tc_fence_after();
-#pragma unroll 1
-      for (int rd = 0; rd < DH / 64; ++rd) {
-        uint32_t u0[32], u1[32];
-        tmem_ld32(tdP + lane_off + rd * 64, u0);
-        tmem_ld32(tdP + lane_off + rd * 64 + 32, u1);
-        tmem_wait_ld();
-        if (rd == DH / 64 - 1) {
-          tc_fence_before();
-          mbar_arrive(tdp_free);
-          if (t == 0) TR(it, 10);
-        }
-        if (rd > 0) {                          // staging reused: previous reduce must have read it
-          if (t == 0) bulk_wait_read0();
-          named_bar(2, 128);
-        }
+      uint32_t u[DH / 32][32];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          *reinterpret_cast<uint4*>(stg + t * 128 + ((j ^ (t & 7)) << 4)) =
-              make_uint4(u0[4 * j], u0[4 * j + 1], u0[4 * j + 2], u0[4 * j + 3]);
-          *reinterpret_cast<uint4*>(stg + ATOM + t * 128 + ((j ^ (t & 7)) << 4)) =
-              make_uint4(u1[4 * j], u1[4 * j + 1], u1[4 * j + 2], u1[4 * j + 3]);
-        }
+      for (int c = 0; c < DH / 32; ++c) tmem_ld32(tdP + lane_off + c * 32, u[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(tdp_free);                   // TMEM columns free for the next dPᵀ
+      if (t == 0) TR(it, 10);
+#pragma unroll
+      for (int rd = 0; rd < DH / 64; ++rd) {
+        if (t == 0) bulk_wait_read0();         // staging buffer read by the previous reduce
+        named_bar(2, 128);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(stg + hh * ATOM + t * 128 + ((j ^ (t & 7)) << 4)) =
+                make_uint4(u[rd * 2 + hh][4 * j], u[rd * 2 + hh][4 * j + 1], u[rd * 2 + hh][4 * j + 2],
+                           u[rd * 2 + hh][4 * j + 3]);
         fence_async_smem();
         named_bar(2, 128);
         if (t == 0) {
@@ -1011,11 +1034,7 @@ __global__ void __launch_bounds__(320, 1)
           bulk_commit();
         }
       }
-      if (t == 0) {
-        bulk_wait_read0();
-        mbar_arrive(dsbuf_free);
-        TR(it, 11);
-      }
+      if (t == 0) TR(it, 11);
     }
     if (t == 0) bulk_wait_all0();
   }
@@ -1028,7 +1047,8 @@ __global__ void __launch_bounds__(320, 1)
 
 // δ_i = Σ_d dO_id·O_id ; one warp per (row, head)
 __global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16* __restrict__ o,
-                                const bf16* __restrict__ dout, float* __restrict__ delta) {
+                                const bf16* __restrict__ dout, float* __restrict__ delta,
+                                const float* __restrict__ lse, float* __restrict__ lse2) {
   const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32;
   const int lane = threadIdx.x % 32;
   if (w >= rows * nh) return;
@@ -1043,7 +1063,11 @@ __global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16*
   }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-  if (lane == 0) delta[(row / S * nh + h) * S + row % S] = acc;
+  if (lane == 0) {
+    const int64_t li = (row / S * nh + h) * S + row % S;
+    delta[li] = acc;
+    lse2[li] = lse[li] * LOG2E;   // log2-domain LSE for the exp2 of the backward
+  }
 }
 
 // dq (bf16, × softmax scale) <- fp32 accumulator
@@ -1140,8 +1164,15 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   TP_CHECK(dq_acc != nullptr, TAWPIPE_ECONFIG, "tcgen05 attention backward needs the fp32 dq accumulator");
   const int H = nh * dh;
   const int64_t rows = static_cast<int64_t>(B) * S;
+  static float* lse2 = nullptr;
+  static int64_t lse2_n = 0;
+  if (lse2_n < rows * nh) {
+    if (lse2) TP_CUDA(cudaFree(lse2));
+    TP_CUDA(cudaMalloc(&lse2, rows * nh * sizeof(float)));
+    lse2_n = rows * nh;
+  }
   fa_delta_kernel<<<static_cast<unsigned>((rows * nh * 32 + 255) / 256), 256, 0, s>>>(rows, S, nh, dh, o, dout,
-                                                                                    delta);
+                                                                                    delta, lse, lse2);
   TP_CUDA(cudaMemsetAsync(dq_acc, 0, rows * H * sizeof(float), s));
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, rows, 3ll * H, 128);
   CUtensorMap tmdo = make_tmap_bf16_2d(dout, H, rows, H, 128);
@@ -1160,12 +1191,12 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   if (dh == 128) {
     static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
                                                                scale2, trace);
   } else {
     static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
                                                              scale2, trace);
   }
   {
@@ -1185,9 +1216,9 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   if (trace) {
     unsigned long long h[32 * 16];
     TP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
-    static const char* names[12] = {"mma:S_issued", "mma:tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
-                                    "cmp:p_done", "cmp:dp_full", "cmp:dsbuf_ok", "cmp:ds_done", "dq:mm2_done",
-                                    "dq:tdp_free", "dq:dsbuf_free"};
+    static const char* names[12] = {"mma:S_issued", "mma:dO+tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
+                                    "cmp:p_done", "cmp:dp_full", "cmp:mm2_prev", "cmp:ds_done", "dq:mm2_done",
+                                    "dq:tdp_free", "dq:staged"};
     const unsigned long long t0 = h[0];
     for (int it = 0; it < 12; ++it) {
       std::fprintf(stderr, "it %2d:", it);

@@ -30,6 +30,35 @@ __global__ void red_coalesced(float* dst, int iters, int ntiles, int H) {
     }
   }
 }
+// 16x256b-like pattern: thread t -> row (t/4) (+8), 2 consecutive columns at 2*(t%4): 4 threads = one 32 B sector
+__global__ void red_sector_v2(float* dst, int iters, int ntiles, int H) {
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;  // 4 warps, warp w owns rows [32w, 32w+32)
+  for (int it = 0; it < iters; ++it) {
+    const int tile = (blockIdx.x + it * gridDim.x) % ntiles;
+#pragma unroll 4
+    for (int half = 0; half < 2; ++half)
+      for (int cg = 0; cg < 16; ++cg)
+        for (int rr = 0; rr < 2; ++rr) {
+          const int row = w * 32 + half * 16 + rr * 8 + lane / 4;
+          float* p = dst + (size_t)(tile * 128 + row) * H + cg * 8 + (lane % 4) * 2;
+          asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1.f), "f"(1.f) : "memory");
+        }
+  }
+}
+// 2 threads x 16 B = 32 B per row, 16 rows per warp instruction
+__global__ void red_sector_v4(float* dst, int iters, int ntiles, int H) {
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  for (int it = 0; it < iters; ++it) {
+    const int tile = (blockIdx.x + it * gridDim.x) % ntiles;
+#pragma unroll 4
+    for (int half = 0; half < 2; ++half)
+      for (int cg = 0; cg < 16; ++cg) {
+        const int row = w * 32 + half * 16 + lane / 2;
+        float* p = dst + (size_t)(tile * 128 + row) * H + cg * 8 + (lane % 2) * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.f), "f"(1.f), "f"(1.f), "f"(1.f) : "memory");
+      }
+  }
+}
 __global__ void tma_red(const __grid_constant__ CUtensorMap tm, int iters, int ntiles) {
   extern __shared__ __align__(1024) uint8_t sm[];
   if (threadIdx.x == 0) {
@@ -59,6 +88,13 @@ int main() {
     // 296 CTAs (2 per SM) variants
     cudaEventRecord(a); red_coalesced<<<296, 128>>>(d, iters / 2, ntiles, H); cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b); printf("red.v4 coalesced x2   : %.1f GB/s\n", bytes / ms / 1e6);
+  }
+  for (int rep = 0; rep < 2; ++rep) {
+    float ms;
+    cudaEventRecord(a); red_sector_v2<<<148, 128>>>(d, iters, ntiles, H); cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b); printf("red.v2 sector (16x256b): %.1f GB/s\n", bytes / ms / 1e6);
+    cudaEventRecord(a); red_sector_v4<<<148, 128>>>(d, iters, ntiles, H); cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b); printf("red.v4 sector pairs   : %.1f GB/s\n", bytes / ms / 1e6);
   }
   PFN_cuTensorMapEncodeTiled_v12000 enc; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", (void**)&enc, 12000, cudaEnableDefault, &q);

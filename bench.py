@@ -43,12 +43,14 @@ CONFIGS = {
 
 
 def flops_per_token(c, recompute=True):
-    """forward 2·φ_dense + 2H(S+1) per layer + 2HV head; train = 3×; + recompute."""
+    """forward 2·φ_dense + 2H(S+1) per layer + 2HV head; train = 3×; + the recompute the step
+    executes (checkpointing recomputes every layer's forward except the last layer's last micro-batch, whose
+    activations are still resident: L − 1/m layers per token)."""
     H, I, S, L, V = c["H"], c["I"], c["S"], c["L"], c["V"]
     layer_fwd = 2 * (4 * H * H + 3 * H * I) + 2 * H * (S + 1)
     f = 3 * (L * layer_fwd + 2 * H * V)
     if recompute and c["ckpt"]:
-        f += L * layer_fwd
+        f += (L - 1.0 / c["m"]) * layer_fwd
     return f
 
 

@@ -730,6 +730,241 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ----------------------------------------------------------------------------------------------- forward v4
+// As v3, but the row softmax is split over two warps per SMSP: warp w (w = 2..9) handles rows 32(w%4).. and
+// key columns 64·h.. (h = half).  The two halves exchange their partial row maxima through smem once per
+// key tile (one named barrier); row sums stay per half until the end.  Each half writes its P columns into
+// its own S columns of TMEM and rescales its half of O.
+//   warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: softmax (half = (w - 2) / 4)
+template <int DH>
+struct Fwd4Smem {
+  static constexpr int QB = DH / 64 * ATOM;
+  static constexpr int NST = 3;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = QB;
+  static constexpr int OFF_V = QB + NST * QB;
+  static constexpr int OFF_RED = QB + 2 * NST * QB;   // [2 buffers][2 halves][128] partial maxima (then sums)
+  static constexpr int OFF_BAR = OFF_RED + 2 * 1024;
+  static constexpr int BYTES = OFF_BAR + 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(320, 1)
+    fa_fwd4_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
+                   int nh, float scale2) {
+  using L = Fwd4Smem<DH>;
+  constexpr int NST = L::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
+           *v_empty = bar + 1 + 3 * NST, *s_full = bar + 1 + 4 * NST, *p_ready = bar + 3 + 4 * NST,
+           *o_done = bar + 5 + 4 * NST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8 + 4 * NST);
+  float* red = reinterpret_cast<float*>(sm + L::OFF_RED);   // red[(buf * 2 + half) * 128 + row]
+
+  const int n_q = S / BQ;
+  // head-major order (the K/V of one head stay in L2 across its query tiles), heaviest tiles first in a head
+  const int qt = n_q - 1 - static_cast<int>(blockIdx.x % n_q);
+  const int h = static_cast<int>(blockIdx.x / n_q);
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int n_kv = qt + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_ready[i], 256);
+    }
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, L::QB);
+      for (int a = 0; a < DH / 64; ++a)
+        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qt * BQ);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % NST;
+        const uint32_t ph = (j / NST) & 1;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
+                      row0 + j * BQ);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
+      const uint32_t sQ = smem_u32(sm + L::OFF_Q);
+      auto issue_s = [&](int j) {
+        const int st = j % NST;
+        mbar_wait(&k_full[st], (j / NST) & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tmem + (j & 1) * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[j & 1]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (n_kv > 1) issue_s(1);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % NST;
+        mbar_wait(&p_ready[j & 1], (j >> 1) & 1);
+        mbar_wait(&v_full[st], (j / NST) & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
+        const uint32_t tP = tmem + (j & 1) * 128;
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)  // P: keys 0..63 at tP[0,32), keys 64..127 at tP[64,96)
+          umma_f16_tmemA(tO, tP + (ks >> 2) * 64 + (ks & 3) * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
+        umma_commit(&v_empty[st]);
+        umma_commit(o_done);
+        if (j + 2 < n_kv) issue_s(j + 2);   // overwrites S/P buffer (j & 1) after P·V_j in issue order
+      }
+    }
+  } else {
+    const int sw = warp - 2;
+    const int hf = sw >> 2;             // key-column half
+    const int q = warp & 3;             // TMEM lane quarter
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    float m2 = -INFINITY, l = 0.f;
+    float s[64];
+    for (int j = 0; j < n_kv; ++j) {
+      const uint32_t tS = tmem + (j & 1) * 128 + lane_off + hf * 64;
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      {
+        uint32_t u0[32], u1[32];
+        tmem_ld32(tS, u0);
+        tmem_ld32(tS + 32, u1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(u0[i]);
+          s[32 + i] = __uint_as_float(u1[i]);
+        }
+      }
+      if (j == qt) {  // diagonal tile only
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (hf * 64 + i > r) s[i] = -INFINITY;
+      }
+      float mxa[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mxa[k] = s[k];
+#pragma unroll
+      for (int i = 8; i < 64; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+      // combine the two halves' maxima (double-buffered by key tile parity)
+      float* rb = red + (j & 1) * 256;
+      rb[hf * 128 + r] = mx;
+      named_bar(1, 256);
+      mx = fmaxf(rb[r], rb[128 + r]) * scale2;
+      if (j == 0) {
+        m2 = mx;
+      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
+        // rescale this half of O: needs P·V_{j-1} complete.  Both halves see the same combined maxima, so
+        // they take the same decision per row; the warp-uniform vote may differ between the two warps of a row,
+        // which only changes whether m2 is refreshed for rows whose max did not grow (alpha = 1 there).
+        mbar_wait(o_done, (j - 1) & 1);
+        tc_fence_after();
+        const float mnew = fmaxf(m2, mx);
+        const float alpha = ex2(m2 - mnew);
+        l *= alpha;
+#pragma unroll 1
+        for (int c = 0; c < DH / 64; ++c) {
+          uint32_t u[32];
+          const uint32_t ta = tO + lane_off + hf * (DH / 2) + c * 32;
+          tmem_ld32(ta, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st32(ta, u);
+        }
+        m2 = mnew;
+      }
+      float sa[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pw[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2(fmaf(s[c * 32 + i], scale2, -m2));
+          const float p1 = ex2(fmaf(s[c * 32 + i + 1], scale2, -m2));
+          sa[i & 7] += p0;
+          sa[(i + 1) & 7] += p1;
+          pw[i / 2] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + c * 16, pw);
+      }
+      l += ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_ready[j & 1]);
+    }
+    mbar_wait(o_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    float* lsum = red + (n_kv & 1) * 256;   // the buffer not read in the last key tile
+    lsum[hf * 128 + r] = l;
+    named_bar(1, 256);
+    const float ltot = lsum[r] + lsum[128 + r];
+    const float inv = 1.f / ltot;
+    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH + hf * (DH / 2);
+#pragma unroll 1
+    for (int c = 0; c < DH / 64; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tO + lane_off + hf * (DH / 2) + c * 32, u);
+      tmem_wait_ld();
+      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 o;
+        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+        d4[v] = o;
+      }
+    }
+    if (hf == 0) lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(ltot)) * (1.0f / LOG2E);
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // =============================================================================================== backward
 // Warp roles (320 threads, one CTA per SM):
 //   warps 0-3  softmax-gradient warps, thread t <-> key row t of the tile (TMEM lane t):
@@ -1104,6 +1339,21 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
     const char* e = std::getenv("TAWPIPE_FA_FWD");
     return e ? std::atoi(e) : 3;
   }();
+  if (fwd_ver == 4) {
+    dim3 grid4(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+    if (dh == 128) {
+      static bool once = (prep(fa_fwd4_kernel<128>, Fwd4Smem<128>::BYTES), true);
+      (void)once;
+      fa_fwd4_kernel<128><<<grid4, 320, Fwd4Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    } else {
+      static bool once = (prep(fa_fwd4_kernel<64>, Fwd4Smem<64>::BYTES), true);
+      (void)once;
+      fa_fwd4_kernel<64><<<grid4, 320, Fwd4Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    }
+    TP_CUDA(cudaGetLastError());
+    g_kstats.launches++;
+    return;
+  }
   if (fwd_ver == 3) {
     static const int emu = [] {
       const char* e = std::getenv("TAWPIPE_FA_EMU");   // exponentials per 8 computed on the FMA pipe
@@ -1117,7 +1367,8 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
     fa_fwd3_kernel<D, E><<<grid3, 192, Fwd3Smem<D>::BYTES, s>>>(tm, o, lse, S, nh, scale2);           \
   } while (0)
     if (dh == 128) {
-      if (emu == 2) FWD3_LAUNCH(128, 2);
+      if (emu == 1) FWD3_LAUNCH(128, 1);
+      else if (emu == 2) FWD3_LAUNCH(128, 2);
       else if (emu == 3) FWD3_LAUNCH(128, 3);
       else if (emu == 4) FWD3_LAUNCH(128, 4);
       else FWD3_LAUNCH(128, 0);

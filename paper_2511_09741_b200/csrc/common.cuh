@@ -64,6 +64,10 @@ struct GemmArgs {
   bool c_f32;
   bool accumulate;
   const void* R;  // residual (same dtype / ld as C), nullable
+  int epi = 0;     // 0 plain, 3 SwiGLU forward (C = gu or null, aux = y), 4 SwiGLU backward (C = dgu, aux = gu)
+  void* aux = nullptr;
+  int64_t ldx = 0;
+  int64_t I = 0;
 };
 void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s);   // tcgen05 + TMA + TMEM
 template <typename T>

@@ -177,17 +177,21 @@ inline ncclDataType_t wire_type() { return g->bf ? ncclBfloat16 : ncclFloat32; }
 inline char* wptr(void* base, int64_t elems) { return static_cast<char*>(base) + elems * static_cast<int64_t>(g->esz); }
 
 // ------------------------------------------------------------------------------------ kernel dispatch
-void gemm(int64_t M, int64_t Nn, int64_t K, const void* A, int64_t lda, bool akm, const void* B, int64_t ldb, bool bkm,
-          void* C, int64_t ldc, bool c_f32, bool acc, const void* R, cudaStream_t s) {
-  GemmArgs a{M, Nn, K, A, lda, akm, B, ldb, bkm, C, ldc, c_f32, acc, R};
-  Timed t(s, 0, 2.0 * M * Nn * K);
+bool gemm_force_simt() {
   static const bool force_simt = [] {
     const char* e = std::getenv("TAWPIPE_GEMM");
     return e && std::string(e) == "simt";
   }();
+  return force_simt;
+}
+
+void gemm(int64_t M, int64_t Nn, int64_t K, const void* A, int64_t lda, bool akm, const void* B, int64_t ldb, bool bkm,
+          void* C, int64_t ldc, bool c_f32, bool acc, const void* R, cudaStream_t s) {
+  GemmArgs a{M, Nn, K, A, lda, akm, B, ldb, bkm, C, ldc, c_f32, acc, R};
+  Timed t(s, 0, 2.0 * M * Nn * K);
   if (!g->bf)
     gemm_simt<float>(a, s);
-  else if (force_simt)
+  else if (gemm_force_simt())
     gemm_simt<bf16>(a, s);
   else
     gemm_tc_bf16(a, s);
@@ -472,8 +476,19 @@ void layer_forward(int l, int mb, void* W, bool write_out) {
   attn_fwd(A.qkv, A.o, A.lse, s);
   gemm(T, H, H, A.o, H, true, w.wo, H, true, A.h1, H, false, false, hin, s);
   k_rmsnorm_fwd(A.h1, w.mlp_norm, A.b, A.r2, T, s);
-  gemm(T, 2 * I, H, A.b, H, true, w.wgu, H, true, A.gu, 2 * I, false, false, nullptr, s);
-  {
+  if (g->bf && !gemm_force_simt()) {
+    // gate/up GEMM with the SwiGLU epilogue: y directly; gu is stored only when a backward will read it
+    // (no checkpointing, the recompute pass, or the last layer's last micro-batch which skips recompute)
+    const bool need_gu = !g->dims.ckpt || !write_out || (l == g->L - 1 && mb == g->m - 1);
+    GemmArgs a{T, 2 * I, H, A.b, H, true, w.wgu, H, true, need_gu ? A.gu : nullptr, 2 * I, false, false, nullptr};
+    a.epi = 3;
+    a.aux = A.y;
+    a.ldx = I;
+    a.I = I;
+    Timed t(s, 0, 2.0 * T * 2 * I * H);
+    gemm_tc_bf16(a, s);
+  } else {
+    gemm(T, 2 * I, H, A.b, H, true, w.wgu, H, true, A.gu, 2 * I, false, false, nullptr, s);
     Timed t(s, 4, 0);
     BY_TYPE(swiglu_fwd<float>((const float*)A.gu, (float*)A.y, T, (int)I, s),
             swiglu_fwd<bf16>((const bf16*)A.gu, (bf16*)A.y, T, (int)I, s));
@@ -485,7 +500,9 @@ void layer_backward(int l, int mb, void* W, float* G_) {
   cudaStream_t s = g->cs;
   const int64_t T = g->T, H = g->H, I = g->I;
   LayerW w = layer_weights(W);
-  if (g->dims.ckpt) layer_forward(l, mb, W, false);  // recompute from the checkpoint h_l
+  // recompute from the checkpoint h_l; the last layer's last micro-batch is still resident in the
+  // scratch activations from the forward pass, so it needs no recompute
+  if (g->dims.ckpt && !(l == g->L - 1 && mb == g->m - 1)) layer_forward(l, mb, W, false);
   Acts& A = acts_for(l, mb);
   void* hin = ck(l, mb);
   void* dh = g->dhb[mb];
@@ -496,8 +513,17 @@ void layer_backward(int l, int mb, void* W, float* G_) {
   float* gd = G_ + 2 * H + 4 * H * H + 2 * I * H;  // Wdown [H, I]
   // h2 = h1 + y·Wdownᵀ
   gemm(H, I, T, dh, H, false, A.y, I, false, gd, I, true, true, nullptr, s);
-  gemm(T, I, H, dh, H, true, w.wdown, I, false, g->dY, I, false, false, nullptr, s);
-  {
+  if (g->bf && !gemm_force_simt()) {
+    // dgrad of the down projection with the SwiGLU backward in the epilogue: dY never reaches HBM
+    GemmArgs a{T, I, H, dh, H, true, w.wdown, I, false, g->dGU, 2 * I, false, false, nullptr};
+    a.epi = 4;
+    a.aux = A.gu;
+    a.ldx = 2 * I;
+    a.I = I;
+    Timed t(s, 0, 2.0 * T * I * H);
+    gemm_tc_bf16(a, s);
+  } else {
+    gemm(T, I, H, dh, H, true, w.wdown, I, false, g->dY, I, false, false, nullptr, s);
     Timed t(s, 4, 0);
     BY_TYPE(swiglu_bwd<float>((const float*)g->dY, (const float*)A.gu, (float*)g->dGU, T, (int)I, s),
             swiglu_bwd<bf16>((const bf16*)g->dY, (const bf16*)A.gu, (bf16*)g->dGU, T, (int)I, s));
@@ -646,7 +672,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
     TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.units[l].n_pad * 4, c.cs));
     void* W = unit_buffer(l, slot);
     TRACE("backward layer %d\n", l);
-    for (int mb = 0; mb < c.m; ++mb) layer_backward(l, mb, W, c.gacc[slot]);
+    for (int mb = c.m - 1; mb >= 0; --mb) layer_backward(l, mb, W, c.gacc[slot]);  // last micro-batch first
     TP_CUDA(cudaEventRecord(c.w_free[slot], c.cs));
     TP_CUDA(cudaEventRecord(c.g_ready[slot], c.cs));
     if (!cco && l - 1 >= 0) {

@@ -39,12 +39,15 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
-enum Epi : int { EPI_BF16 = 0, EPI_F32_STORE = 1, EPI_F32_ACC = 2 };
+enum Epi : int { EPI_BF16 = 0, EPI_F32_STORE = 1, EPI_F32_ACC = 2, EPI_SWIGLU_FWD = 3, EPI_SWIGLU_BWD = 4 };
+
+__device__ __forceinline__ float silu_sig(float u) { return 1.f / (1.f + __expf(-u)); }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
-                   int64_t ldc, const bf16* __restrict__ R, int M, int N, int K) {
+                   int64_t ldc, const bf16* __restrict__ R, int M, int N, int K, void* __restrict__ aux, int64_t ldx,
+                   int64_t I) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -108,7 +111,10 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i) tma_load_2d(sa + i * 8192, &tmA, &full[stage], mb * BM + i * 64, kb * BK);
           }
-          if (!B_MN) {
+          if (EPI == EPI_SWIGLU_FWD) {  // B tile = 128 gate rows + the matching 128 up rows of [Wgate; Wup]
+            tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * (BN / 2));
+            tma_load_2d(sb + (BN / 2) * 128, &tmB, &full[stage], kb * BK, static_cast<int>(I) + nb * (BN / 2));
+          } else if (!B_MN) {
             tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * BN);
           } else {
 #pragma unroll
@@ -166,51 +172,124 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int64_t row = static_cast<int64_t>(mb) * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      if (EPI == EPI_SWIGLU_FWD) {
+        // accumulator columns [0, BN/2) = gate u, [BN/2, BN) = up w of output features nb·BN/2 ..:
+        // y = SiLU(u)·w -> aux [rows, I] ; optionally (C != nullptr) u, w -> C = gu [rows, 2I]
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tbase + c, r);
-        tmem_wait_ld();
-        const int64_t col = static_cast<int64_t>(nb) * BN + c;
-        if (EPI == EPI_BF16) {
-          bf16* dst = reinterpret_cast<bf16*>(C) + row * ldc + col;
-          float f[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
-          if (R != nullptr) {
-            const uint4* rs = reinterpret_cast<const uint4*>(R + row * ldc + col);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 x = rs[v];
-              const bf16* xb = reinterpret_cast<const bf16*>(&x);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) f[v * 8 + i] += __bfloat162float(xb[i]);
-            }
-          }
-          uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t ru[32], rw[32];
+          tmem_ld32(tbase + c, ru);
+          tmem_ld32(tbase + BN / 2 + c, rw);
+          tmem_wait_ld();
+          const int64_t col = static_cast<int64_t>(nb) * (BN / 2) + c;
+          uint4* y4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(aux) + row * ldx + col);
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            uint4 o;
-            o.x = pack_bf16(f[v * 8 + 0], f[v * 8 + 1]);
-            o.y = pack_bf16(f[v * 8 + 2], f[v * 8 + 3]);
-            o.z = pack_bf16(f[v * 8 + 4], f[v * 8 + 5]);
-            o.w = pack_bf16(f[v * 8 + 6], f[v * 8 + 7]);
-            d4[v] = o;
-          }
-        } else {
-          float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + row * ldc + col);
+            float yv[8];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-            if (EPI == EPI_F32_ACC) {
-              const float4 p = d4[v];
-              o.x += p.x;
-              o.y += p.y;
-              o.z += p.z;
-              o.w += p.w;
+            for (int e = 0; e < 8; ++e) {
+              const float u = __uint_as_float(ru[v * 8 + e]), w = __uint_as_float(rw[v * 8 + e]);
+              yv[e] = u * silu_sig(u) * w;
             }
-            d4[v] = o;
+            y4[v] = make_uint4(pack_bf16(yv[0], yv[1]), pack_bf16(yv[2], yv[3]), pack_bf16(yv[4], yv[5]),
+                               pack_bf16(yv[6], yv[7]));
+          }
+          if (C != nullptr) {
+            uint4* u4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + col);
+            uint4* w4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + I + col);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              u4[v] = make_uint4(pack_bf16(__uint_as_float(ru[8 * v]), __uint_as_float(ru[8 * v + 1])),
+                                 pack_bf16(__uint_as_float(ru[8 * v + 2]), __uint_as_float(ru[8 * v + 3])),
+                                 pack_bf16(__uint_as_float(ru[8 * v + 4]), __uint_as_float(ru[8 * v + 5])),
+                                 pack_bf16(__uint_as_float(ru[8 * v + 6]), __uint_as_float(ru[8 * v + 7])));
+              w4[v] = make_uint4(pack_bf16(__uint_as_float(rw[8 * v]), __uint_as_float(rw[8 * v + 1])),
+                                 pack_bf16(__uint_as_float(rw[8 * v + 2]), __uint_as_float(rw[8 * v + 3])),
+                                 pack_bf16(__uint_as_float(rw[8 * v + 4]), __uint_as_float(rw[8 * v + 5])),
+                                 pack_bf16(__uint_as_float(rw[8 * v + 6]), __uint_as_float(rw[8 * v + 7])));
+            }
+          }
+        }
+      } else if (EPI == EPI_SWIGLU_BWD) {
+        // accumulator = dy = dh·Wdown for features nb·BN ..: du = dy·w·σ(u)(1 + u(1−σ(u))), dw = dy·SiLU(u)
+        // with u, w read from aux = gu [rows, 2I]; writes C = dgu [rows, 2I]
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          const int64_t col = static_cast<int64_t>(nb) * BN + c;
+          const uint4* gu4 = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(aux) + row * ldx + col);
+          const uint4* gw4 = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(aux) + row * ldx + I + col);
+          uint4* du4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + col);
+          uint4* dw4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + I + col);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint4 ux = gu4[v], wx = gw4[v];
+            const bf16* ub = reinterpret_cast<const bf16*>(&ux);
+            const bf16* wb = reinterpret_cast<const bf16*>(&wx);
+            float du[8], dw[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float u = __bfloat162float(ub[e]), w = __bfloat162float(wb[e]);
+              const float dy = __uint_as_float(r[v * 8 + e]);
+              const float sg = silu_sig(u);
+              du[e] = dy * w * sg * (1.f + u * (1.f - sg));
+              dw[e] = dy * u * sg;
+            }
+            du4[v] = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]), pack_bf16(du[4], du[5]),
+                                pack_bf16(du[6], du[7]));
+            dw4[v] = make_uint4(pack_bf16(dw[0], dw[1]), pack_bf16(dw[2], dw[3]), pack_bf16(dw[4], dw[5]),
+                                pack_bf16(dw[6], dw[7]));
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c, r);
+          tmem_wait_ld();
+          const int64_t col = static_cast<int64_t>(nb) * BN + c;
+          if (EPI == EPI_BF16) {
+            bf16* dst = reinterpret_cast<bf16*>(C) + row * ldc + col;
+            float f[32];
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+            if (R != nullptr) {
+              const uint4* rs = reinterpret_cast<const uint4*>(R + row * ldc + col);
+  #pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint4 x = rs[v];
+                const bf16* xb = reinterpret_cast<const bf16*>(&x);
+  #pragma unroll
+                for (int i = 0; i < 8; ++i) f[v * 8 + i] += __bfloat162float(xb[i]);
+              }
+            }
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+  #pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 o;
+              o.x = pack_bf16(f[v * 8 + 0], f[v * 8 + 1]);
+              o.y = pack_bf16(f[v * 8 + 2], f[v * 8 + 3]);
+              o.z = pack_bf16(f[v * 8 + 4], f[v * 8 + 5]);
+              o.w = pack_bf16(f[v * 8 + 6], f[v * 8 + 7]);
+              d4[v] = o;
+            }
+          } else {
+            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + row * ldc + col);
+  #pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                     __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+              if (EPI == EPI_F32_ACC) {
+                const float4 p = d4[v];
+                o.x += p.x;
+                o.y += p.y;
+                o.z += p.z;
+                o.w += p.w;
+              }
+              d4[v] = o;
+            }
           }
         }
       }
@@ -290,18 +369,25 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   }
   // A: K-major -> rows M, inner K ; MN-major -> inner M, rows K
   CUtensorMap ta = A_MN ? make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, 64) : make_tmap_bf16_2d(g.A, g.K, g.M, g.lda, BM);
-  CUtensorMap tb = B_MN ? make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 64) : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, BN);
+  CUtensorMap tb = B_MN ? make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 64)
+                        : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, EPI == EPI_SWIGLU_FWD ? BN / 2 : BN);
   const int tiles = static_cast<int>((g.M / BM) * (g.N / BN));
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
-                                     static_cast<int>(g.N), static_cast<int>(g.K));
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }
 
 template <int BN, bool A_MN, bool B_MN>
 void dispatch_epi(const GemmArgs& g, cudaStream_t s) {
-  if (!g.c_f32)
+  if (g.epi == 3) {
+    if constexpr (!A_MN && !B_MN) launch<BN, A_MN, B_MN, EPI_SWIGLU_FWD>(g, s);
+    else throw Error(TAWPIPE_ECONFIG, "SwiGLU forward epilogue needs K-major operands");
+  } else if (g.epi == 4) {
+    if constexpr (!A_MN && B_MN) launch<BN, A_MN, B_MN, EPI_SWIGLU_BWD>(g, s);
+    else throw Error(TAWPIPE_ECONFIG, "SwiGLU backward epilogue is the dgrad form (A K-major, B MN-major)");
+  } else if (!g.c_f32)
     launch<BN, A_MN, B_MN, EPI_BF16>(g, s);
   else if (g.accumulate)
     launch<BN, A_MN, B_MN, EPI_F32_ACC>(g, s);
@@ -325,6 +411,11 @@ void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
            "tcgen05 GEMM needs M%128==0, N%128==0, K%64==0 (got " + std::to_string(g.M) + "x" +
                std::to_string(g.N) + "x" + std::to_string(g.K) + ")");
   TP_CHECK(!(g.accumulate && !g.c_f32), TAWPIPE_ECONFIG, "bf16 accumulate-into-C is not supported; use R");
+  if (g.epi == 3) {  // the gate/up tile pairs 128 gate rows with 128 up rows: always BN = 256
+    TP_CHECK(g.N % 256 == 0 && g.I * 2 == g.N && g.aux, TAWPIPE_ECONFIG, "SwiGLU forward: N = 2I, I % 128 == 0");
+    dispatch_major<256>(g, s);
+    return;
+  }
   TP_CHECK(!(g.R && g.c_f32), TAWPIPE_ECONFIG, "residual only with bf16 C");
   TP_CHECK((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B) | reinterpret_cast<uintptr_t>(g.C)) %
                    16 == 0 &&

@@ -1,5 +1,5 @@
 #!/bin/bash
-# forward-attention variants at the C3 shape (3 timed iterations each)
-for cfg in "TAWPIPE_FA_FWD=3 TAWPIPE_FA_EMU=0" "TAWPIPE_FA_FWD=3 TAWPIPE_FA_EMU=2" "TAWPIPE_FA_FWD=3 TAWPIPE_FA_EMU=3" "TAWPIPE_FA_FWD=3 TAWPIPE_FA_EMU=4" "TAWPIPE_FA_FWD=2" "TAWPIPE_FA_FWD=1"; do
-  echo "== $cfg"; env $cfg timeout 120 python tools/attn_big.py 32768 32 2>&1 | head -3
+# forward-attention exp-emulation sweep at the C3 shape (fwd only matters; 3 timed iterations each)
+for e in 0 1 2 3 0; do
+  echo "== EMU=$e"; TAWPIPE_FA_EMU=$e timeout 120 python tools/attn_big.py 32768 32 2>&1 | head -3 | cut -c 1-45
 done

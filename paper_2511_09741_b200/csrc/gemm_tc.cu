@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -43,6 +44,135 @@ struct GemmCfg {
 enum Epi : int { EPI_BF16 = 0, EPI_F32_STORE = 1, EPI_F32_ACC = 2, EPI_SWIGLU_FWD = 3, EPI_SWIGLU_BWD = 4 };
 
 __device__ __forceinline__ float silu_sig(float u) { return 1.f / (1.f + __expf(-u)); }
+
+// Epilogue of one output tile for this thread's accumulator row: TMEM columns [0, BN) of `tbase` hold
+// C[row, nb·BN ..) (SwiGLU forward: gate u in [0, BN/2), up w in [BN/2, BN) of features nb·BN/2 ..).
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(uint32_t tbase, int64_t row, int nb, void* __restrict__ C, int64_t ldc,
+                                              const bf16* __restrict__ R, void* __restrict__ aux, int64_t ldx,
+                                              int64_t I) {
+  if (EPI == EPI_SWIGLU_FWD) {
+    // accumulator columns [0, BN/2) = gate u, [BN/2, BN) = up w of output features nb·BN/2 ..:
+    // y = SiLU(u)·w -> aux [rows, I] ; optionally (C != nullptr) u, w -> C = gu [rows, 2I]
+#pragma unroll 1
+    for (int c = 0; c < BN / 2; c += 32) {
+      uint32_t ru[32], rw[32];
+      tmem_ld32(tbase + c, ru);
+      tmem_ld32(tbase + BN / 2 + c, rw);
+      tmem_wait_ld();
+      const int64_t col = static_cast<int64_t>(nb) * (BN / 2) + c;
+      uint4* y4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(aux) + row * ldx + col);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        float yv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float u = __uint_as_float(ru[v * 8 + e]), w = __uint_as_float(rw[v * 8 + e]);
+          yv[e] = u * silu_sig(u) * w;
+        }
+        y4[v] = make_uint4(pack_bf16(yv[0], yv[1]), pack_bf16(yv[2], yv[3]), pack_bf16(yv[4], yv[5]),
+                           pack_bf16(yv[6], yv[7]));
+      }
+      if (C != nullptr) {
+        uint4* u4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + col);
+        uint4* w4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + I + col);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          u4[v] = make_uint4(pack_bf16(__uint_as_float(ru[8 * v]), __uint_as_float(ru[8 * v + 1])),
+                             pack_bf16(__uint_as_float(ru[8 * v + 2]), __uint_as_float(ru[8 * v + 3])),
+                             pack_bf16(__uint_as_float(ru[8 * v + 4]), __uint_as_float(ru[8 * v + 5])),
+                             pack_bf16(__uint_as_float(ru[8 * v + 6]), __uint_as_float(ru[8 * v + 7])));
+          w4[v] = make_uint4(pack_bf16(__uint_as_float(rw[8 * v]), __uint_as_float(rw[8 * v + 1])),
+                             pack_bf16(__uint_as_float(rw[8 * v + 2]), __uint_as_float(rw[8 * v + 3])),
+                             pack_bf16(__uint_as_float(rw[8 * v + 4]), __uint_as_float(rw[8 * v + 5])),
+                             pack_bf16(__uint_as_float(rw[8 * v + 6]), __uint_as_float(rw[8 * v + 7])));
+        }
+      }
+    }
+  } else if (EPI == EPI_SWIGLU_BWD) {
+    // accumulator = dy = dh·Wdown for features nb·BN ..: du = dy·w·σ(u)(1 + u(1−σ(u))), dw = dy·SiLU(u)
+    // with u, w read from aux = gu [rows, 2I]; writes C = dgu [rows, 2I]
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tbase + c, r);
+      tmem_wait_ld();
+      const int64_t col = static_cast<int64_t>(nb) * BN + c;
+      const uint4* gu4 = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(aux) + row * ldx + col);
+      const uint4* gw4 = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(aux) + row * ldx + I + col);
+      uint4* du4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + col);
+      uint4* dw4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + I + col);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 ux = gu4[v], wx = gw4[v];
+        const bf16* ub = reinterpret_cast<const bf16*>(&ux);
+        const bf16* wb = reinterpret_cast<const bf16*>(&wx);
+        float du[8], dw[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float u = __bfloat162float(ub[e]), w = __bfloat162float(wb[e]);
+          const float dy = __uint_as_float(r[v * 8 + e]);
+          const float sg = silu_sig(u);
+          du[e] = dy * w * sg * (1.f + u * (1.f - sg));
+          dw[e] = dy * u * sg;
+        }
+        du4[v] = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]), pack_bf16(du[4], du[5]),
+                            pack_bf16(du[6], du[7]));
+        dw4[v] = make_uint4(pack_bf16(dw[0], dw[1]), pack_bf16(dw[2], dw[3]), pack_bf16(dw[4], dw[5]),
+                            pack_bf16(dw[6], dw[7]));
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld32(tbase + c, r);
+      tmem_wait_ld();
+      const int64_t col = static_cast<int64_t>(nb) * BN + c;
+      if (EPI == EPI_BF16) {
+        bf16* dst = reinterpret_cast<bf16*>(C) + row * ldc + col;
+        float f[32];
+  #pragma unroll
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+        if (R != nullptr) {
+          const uint4* rs = reinterpret_cast<const uint4*>(R + row * ldc + col);
+  #pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 x = rs[v];
+            const bf16* xb = reinterpret_cast<const bf16*>(&x);
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) f[v * 8 + i] += __bfloat162float(xb[i]);
+          }
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+  #pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 o;
+          o.x = pack_bf16(f[v * 8 + 0], f[v * 8 + 1]);
+          o.y = pack_bf16(f[v * 8 + 2], f[v * 8 + 3]);
+          o.z = pack_bf16(f[v * 8 + 4], f[v * 8 + 5]);
+          o.w = pack_bf16(f[v * 8 + 6], f[v * 8 + 7]);
+          d4[v] = o;
+        }
+      } else {
+        float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + row * ldc + col);
+  #pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          if (EPI == EPI_F32_ACC) {
+            const float4 p = d4[v];
+            o.x += p.x;
+            o.y += p.y;
+            o.z += p.z;
+            o.w += p.w;
+          }
+          d4[v] = o;
+        }
+      }
+    }
+  }
+}
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(192, 1)
@@ -173,127 +303,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int64_t row = static_cast<int64_t>(mb) * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      if (EPI == EPI_SWIGLU_FWD) {
-        // accumulator columns [0, BN/2) = gate u, [BN/2, BN) = up w of output features nb·BN/2 ..:
-        // y = SiLU(u)·w -> aux [rows, I] ; optionally (C != nullptr) u, w -> C = gu [rows, 2I]
-#pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-          uint32_t ru[32], rw[32];
-          tmem_ld32(tbase + c, ru);
-          tmem_ld32(tbase + BN / 2 + c, rw);
-          tmem_wait_ld();
-          const int64_t col = static_cast<int64_t>(nb) * (BN / 2) + c;
-          uint4* y4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(aux) + row * ldx + col);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            float yv[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float u = __uint_as_float(ru[v * 8 + e]), w = __uint_as_float(rw[v * 8 + e]);
-              yv[e] = u * silu_sig(u) * w;
-            }
-            y4[v] = make_uint4(pack_bf16(yv[0], yv[1]), pack_bf16(yv[2], yv[3]), pack_bf16(yv[4], yv[5]),
-                               pack_bf16(yv[6], yv[7]));
-          }
-          if (C != nullptr) {
-            uint4* u4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + col);
-            uint4* w4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + I + col);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              u4[v] = make_uint4(pack_bf16(__uint_as_float(ru[8 * v]), __uint_as_float(ru[8 * v + 1])),
-                                 pack_bf16(__uint_as_float(ru[8 * v + 2]), __uint_as_float(ru[8 * v + 3])),
-                                 pack_bf16(__uint_as_float(ru[8 * v + 4]), __uint_as_float(ru[8 * v + 5])),
-                                 pack_bf16(__uint_as_float(ru[8 * v + 6]), __uint_as_float(ru[8 * v + 7])));
-              w4[v] = make_uint4(pack_bf16(__uint_as_float(rw[8 * v]), __uint_as_float(rw[8 * v + 1])),
-                                 pack_bf16(__uint_as_float(rw[8 * v + 2]), __uint_as_float(rw[8 * v + 3])),
-                                 pack_bf16(__uint_as_float(rw[8 * v + 4]), __uint_as_float(rw[8 * v + 5])),
-                                 pack_bf16(__uint_as_float(rw[8 * v + 6]), __uint_as_float(rw[8 * v + 7])));
-            }
-          }
-        }
-      } else if (EPI == EPI_SWIGLU_BWD) {
-        // accumulator = dy = dh·Wdown for features nb·BN ..: du = dy·w·σ(u)(1 + u(1−σ(u))), dw = dy·SiLU(u)
-        // with u, w read from aux = gu [rows, 2I]; writes C = dgu [rows, 2I]
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c, r);
-          tmem_wait_ld();
-          const int64_t col = static_cast<int64_t>(nb) * BN + c;
-          const uint4* gu4 = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(aux) + row * ldx + col);
-          const uint4* gw4 = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(aux) + row * ldx + I + col);
-          uint4* du4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + col);
-          uint4* dw4 = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(C) + row * ldc + I + col);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const uint4 ux = gu4[v], wx = gw4[v];
-            const bf16* ub = reinterpret_cast<const bf16*>(&ux);
-            const bf16* wb = reinterpret_cast<const bf16*>(&wx);
-            float du[8], dw[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float u = __bfloat162float(ub[e]), w = __bfloat162float(wb[e]);
-              const float dy = __uint_as_float(r[v * 8 + e]);
-              const float sg = silu_sig(u);
-              du[e] = dy * w * sg * (1.f + u * (1.f - sg));
-              dw[e] = dy * u * sg;
-            }
-            du4[v] = make_uint4(pack_bf16(du[0], du[1]), pack_bf16(du[2], du[3]), pack_bf16(du[4], du[5]),
-                                pack_bf16(du[6], du[7]));
-            dw4[v] = make_uint4(pack_bf16(dw[0], dw[1]), pack_bf16(dw[2], dw[3]), pack_bf16(dw[4], dw[5]),
-                                pack_bf16(dw[6], dw[7]));
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c, r);
-          tmem_wait_ld();
-          const int64_t col = static_cast<int64_t>(nb) * BN + c;
-          if (EPI == EPI_BF16) {
-            bf16* dst = reinterpret_cast<bf16*>(C) + row * ldc + col;
-            float f[32];
-  #pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
-            if (R != nullptr) {
-              const uint4* rs = reinterpret_cast<const uint4*>(R + row * ldc + col);
-  #pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                uint4 x = rs[v];
-                const bf16* xb = reinterpret_cast<const bf16*>(&x);
-  #pragma unroll
-                for (int i = 0; i < 8; ++i) f[v * 8 + i] += __bfloat162float(xb[i]);
-              }
-            }
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-  #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint4 o;
-              o.x = pack_bf16(f[v * 8 + 0], f[v * 8 + 1]);
-              o.y = pack_bf16(f[v * 8 + 2], f[v * 8 + 3]);
-              o.z = pack_bf16(f[v * 8 + 4], f[v * 8 + 5]);
-              o.w = pack_bf16(f[v * 8 + 6], f[v * 8 + 7]);
-              d4[v] = o;
-            }
-          } else {
-            float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(C) + row * ldc + col);
-  #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                     __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-              if (EPI == EPI_F32_ACC) {
-                const float4 p = d4[v];
-                o.x += p.x;
-                o.y += p.y;
-                o.z += p.z;
-                o.w += p.w;
-              }
-              d4[v] = o;
-            }
-          }
-        }
-      }
+      epilogue_tile<BN, EPI>(tbase, row, nb, C, ldc, R, aux, ldx, I);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -303,6 +313,182 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 5) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------- CTA-pair variant (cta_group::2)
+// A cluster of two CTAs on neighbouring SMs computes one 256×256 output tile with tcgen05.mma.cta_group::2
+// (M = 256, N = 256, K = 16), issued by one thread of the even ("leader") CTA.  Each CTA stages only its own 128
+// rows of A and its half of the 256 B rows (columns of C), so per SM the smem operand traffic per FLOP and the
+// L2 → smem bytes per FLOP both drop by a third against the single-CTA 128×256 tile; each CTA's TMEM holds its
+// 128 rows × 256 columns of the accumulator (two accumulators, 512 columns).
+//   both CTAs: warp 4 TMA producer into own smem, completion counted on the LEADER's full barrier
+//              (the leader's producer posts the expected bytes of both halves);
+//              warps 0-3 epilogue on own TMEM, releasing the accumulator on the leader's tempty (8 arrivals)
+//   leader:    warp 5 lane 0 issues the pair MMAs; tcgen05.commit multicasts smem-stage release (empty) and
+//              accumulator-ready (tfull) to both CTAs
+struct Gemm2Cfg {
+  static constexpr int BN = 256;                      // pair tile N
+  static constexpr int STAGES = 6;
+  static constexpr int A_BYTES = BM * BK * 2;         // 16 KB: this CTA's 128 rows of A
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's half of the B tile
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    void* __restrict__ C, int64_t ldc, const bf16* __restrict__ R, int M, int N, int K,
+                    void* __restrict__ aux, int64_t ldx, int64_t I) {
+  using Cfg = Gemm2Cfg;
+  constexpr int BN = Cfg::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + Cfg::STAGES;
+  uint64_t* tfull = bars + 2 * Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int num_m = M / (2 * BM), num_n = N / BN, num_k = K / BK;
+  const int num_tiles = num_m * num_n;
+  const int cl = blockIdx.x >> 1, n_cl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < Cfg::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc_cg2(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();   // barriers of both CTAs initialised before any remote arrival
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& mb, int& nb) {
+    constexpr int GROUP = 8;   // 8 pair tiles = 2048 rows share each sweep over N
+    const int group_size = GROUP * num_n;
+    const int g = t / group_size;
+    const int first_m = g * GROUP;
+    const int gm = min(GROUP, num_m - first_m);
+    const int r = t % group_size;
+    mb = first_m + r % gm;
+    nb = r / gm;
+  };
+
+  if (warp == 4) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cl; t < num_tiles; t += n_cl) {
+        int mb, nb;
+        tile_coords(t, mb, nb);
+        const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
+        const int n0 = EPI == EPI_SWIGLU_FWD ? (rank ? static_cast<int>(I) : 0) + nb * (BN / 2)
+                                             : nb * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          const uint32_t bar = mapa_shared(&full[stage], 0);
+          if (!A_MN) {
+            tma_load_2d_cg2(sa, &tmA, bar, kb * BK, m0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i) tma_load_2d_cg2(sa + i * 8192, &tmA, bar, m0 + i * 64, kb * BK);
+          }
+          if (!B_MN) {
+            tma_load_2d_cg2(sb, &tmB, bar, kb * BK, n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 128; ++i) tma_load_2d_cg2(sb + i * 8192, &tmB, bar, n0 + i * 64, kb * BK);
+          }
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      // drain: every stage's last release (a multicast commit from the leader) has landed before exit
+      for (int i = 0; i < Cfg::STAGES; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cl; t < num_tiles; t += n_cl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(sa + k * 2048, 8192, 1024) : umma_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(sb + k * 2048, 8192, 1024) : umma_desc_sw128(sb + k * 32, 16, 1024);
+            umma_f16_cg2(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit_cg2(&empty[stage], 0x3);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_cg2(&tfull[acc], 0x3);
+      }
+      // drain: both accumulators released by both CTAs' epilogues (remote arrivals landed) before exit
+      for (int i = 0; i < 2; ++i, ++it) mbar_wait(&tempty[it & 1], ((it >> 1) & 1) ^ 1);
+    }
+  } else {
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = cl; t < num_tiles; t += n_cl, ++it) {
+      int mb, nb;
+      tile_coords(t, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(mb) * 2 * BM + rank * BM + q * 32 + lane;
+      const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      epilogue_tile<BN, EPI>(tbase, row, nb, C, ldc, R, aux, ldx, I);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
@@ -405,6 +591,74 @@ void dispatch_major(const GemmArgs& g, cudaStream_t s) {
   else dispatch_epi<BN, true, false>(g, s);
 }
 
+
+
+template <bool A_MN, bool B_MN, int EPI>
+void launch2(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = Gemm2Cfg;
+  auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  static int max_clusters = 0;
+  if (!attr_set) {
+    TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 148);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0) {
+      (void)cudaGetLastError();
+      max_clusters = 0;
+    }
+    attr_set = true;
+  }
+  if (g_num_sms == 0) {
+    int dev;
+    TP_CUDA(cudaGetDevice(&dev));
+    TP_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int clusters_fit = max_clusters > 0 ? max_clusters : g_num_sms / 2;
+  CUtensorMap ta = A_MN ? make_tmap_bf16_2d(g.A, g.M, g.K, g.lda, 64) : make_tmap_bf16_2d(g.A, g.K, g.M, g.lda, BM);
+  CUtensorMap tb = B_MN ? make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 64) : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, Cfg::BN / 2);
+  const int tiles = static_cast<int>((g.M / (2 * BM)) * (g.N / Cfg::BN));
+  const int grid = 2 * (tiles < clusters_fit ? tiles : clusters_fit);
+  kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I);
+  TP_CUDA(cudaGetLastError());
+  g_kstats.launches++;
+}
+
+template <bool A_MN, bool B_MN>
+void dispatch_epi2(const GemmArgs& g, cudaStream_t s) {
+  if (g.epi == 3) {
+    if constexpr (!A_MN && !B_MN) launch2<A_MN, B_MN, EPI_SWIGLU_FWD>(g, s);
+  } else if (g.epi == 4) {
+    if constexpr (!A_MN && B_MN) launch2<A_MN, B_MN, EPI_SWIGLU_BWD>(g, s);
+  } else if (!g.c_f32)
+    launch2<A_MN, B_MN, EPI_BF16>(g, s);
+  else if (g.accumulate)
+    launch2<A_MN, B_MN, EPI_F32_ACC>(g, s);
+  else
+    launch2<A_MN, B_MN, EPI_F32_STORE>(g, s);
+}
+
+bool use_pair(const GemmArgs& g) {
+  static const int mode = [] {
+    const char* e = getenv("TAWPIPE_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  if (mode == 0 || g.M % (2 * BM) != 0 || g.N % 256 != 0) return false;
+  if (g.epi == 3 && (g.a_kmajor == false || g.b_kmajor == false)) return false;
+  if (g.epi == 4 && !(g.a_kmajor && !g.b_kmajor)) return false;
+  return true;
+}
+
+void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
+  const bool a_mn = !g.a_kmajor, b_mn = !g.b_kmajor;
+  if (!a_mn && !b_mn) dispatch_epi2<false, false>(g, s);
+  else if (!a_mn && b_mn) dispatch_epi2<false, true>(g, s);
+  else if (a_mn && b_mn) dispatch_epi2<true, true>(g, s);
+  else dispatch_epi2<true, false>(g, s);
+}
 }  // namespace
 
 void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
@@ -414,7 +668,8 @@ void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
   TP_CHECK(!(g.accumulate && !g.c_f32), TAWPIPE_ECONFIG, "bf16 accumulate-into-C is not supported; use R");
   if (g.epi == 3) {  // the gate/up tile pairs 128 gate rows with 128 up rows: always BN = 256
     TP_CHECK(g.N % 256 == 0 && g.I * 2 == g.N && g.aux, TAWPIPE_ECONFIG, "SwiGLU forward: N = 2I, I % 128 == 0");
-    dispatch_major<256>(g, s);
+    if (use_pair(g)) dispatch_pair(g, s);
+    else dispatch_major<256>(g, s);
     return;
   }
   TP_CHECK(!(g.R && g.c_f32), TAWPIPE_ECONFIG, "residual only with bf16 C");
@@ -422,7 +677,9 @@ void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
                    16 == 0 &&
                g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0,
            TAWPIPE_ECONFIG, "tcgen05 GEMM needs 16-byte aligned operands and leading dimensions");
-  if (g.N % 256 == 0)
+  if (use_pair(g))
+    dispatch_pair(g, s);
+  else if (g.N % 256 == 0)
     dispatch_major<256>(g, s);
   else
     dispatch_major<128>(g, s);

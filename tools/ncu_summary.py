@@ -11,6 +11,7 @@ KEYS = [("gpu__time_duration.sum", "ms"), ("sm__pipe_tensor_cycles_active.avg.pc
         ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lsu%"),
         ("dram__bytes_read.sum", "dram_rd"), ("dram__bytes_write.sum", "dram_wr"),
         ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%"),
+        ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2%"), ("lts__t_bytes.sum", "l2_bytes"),
         ("sm__cycles_elapsed.avg.per_second", "clk"), ("launch__registers_per_thread", "regs")]
 
 

@@ -43,9 +43,10 @@ CONFIGS = {
 
 
 def flops_per_token(c, recompute=True):
-    """forward 2·φ_dense + 2H(S+1) per layer + 2HV head; train = 3×; + the recompute the step
-    executes (checkpointing recomputes every layer's forward except the last layer's last micro-batch, whose
-    activations are still resident: L − 1/m layers per token)."""
+    """forward 2·φ_dense + 2H(S+1) per layer + 2HV head; train = 3×; + a full recompute
+    (checkpointing recomputes every layer's forward except the last layer's last micro-batch, whose activations
+    are still resident: L − 1/m layers per token).  The step's executed recompute work is smaller when selective
+    checkpointing keeps activations; it is reported by the library (stats recompute_gflop) and used instead."""
     H, I, S, L, V = c["H"], c["I"], c["S"], c["L"], c["V"]
     layer_fwd = 2 * (4 * H * H + 3 * H * I) + 2 * H * (S + 1)
     f = 3 * (L * layer_fwd + 2 * H * V)
@@ -255,7 +256,9 @@ def run_ours(args, c):
         dom, ach, dom_ms = "causal attention fwd+bwd", attn_tf, st["attn_ms"]
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     wire = 2 if c["dtype"] == 1 else 4
-    step_roof_ms = max(flops_per_token(c) * c["m"] * c["B"] * c["S"] / (peaks["bf16_tflops"] * 1e12) * 1e3,
+    rec_gflop = st.get("recompute_gflop", 0.0)    # executed recompute work (selective checkpointing skips kept parts)
+    step_flops = flops_per_token(c, recompute=False) * c["m"] * c["B"] * c["S"] + rec_gflop * 1e9
+    step_roof_ms = max(step_flops / (peaks["bf16_tflops"] * 1e12) * 1e3,
                        max(sum(ledger[i] for i in range(24) if (i // 3) % 2 == 0),
                            sum(ledger[i] for i in range(24) if (i // 3) % 2 == 1)) * wire / 770e9 * 1e3)
     wsz = 2 if c["dtype"] == 1 else 4
@@ -275,9 +278,20 @@ def run_ours(args, c):
         "config": {"workload": config_name(args, c), "model": c["model"], "global_batch": N * c["B"],
                    "seq_len": c["S"], "parallelism": f"tawpipe {world // G}x{G} (D x G)",
                    "l2": "inputs and weights far larger than L2 (no flush needed)",
-                   "schedule": "no-CCO ablation" if args.no_cco else "GWPS+DBS+CCO"},
+                   "schedule": "no-CCO ablation" if args.no_cco else "GWPS+DBS+CCO",
+                   "checkpointing": (f"selective: residual stream + kept activations while memory allows; "
+                                     f"recompute executed {rec_gflop / 1e3:.1f} TFLOP of "
+                                     f"{(flops_per_token(c) - flops_per_token(c, recompute=False)) * c['m'] * c['B'] * c['S'] / 1e12:.1f}")
+                                    if c["ckpt"] else "none"},
         "exposed_comm_ms": exposed, "exposed_comm_frac": exposed / ms, "comm": comm,
         "step_roofline_frac": step_roof_ms / ms,
+        # SURVEY.md §8(d) conventions: the step roofline on the executed work (above), on model FLOPs only (MFU,
+        # no recompute) and on model FLOPs + a full checkpoint recompute (the survey table's HFU figure)
+        "step_roofline_fracs": {
+            "executed_work": step_roof_ms / ms,
+            "mfu_no_recompute": flops_per_token(c, recompute=False) * c["m"] * c["B"] * c["S"]
+            / (peaks["bf16_tflops"] * 1e12) * 1e3 / ms,
+            "hfu_full_recompute": flops_per_token(c) * c["m"] * c["B"] * c["S"] / (peaks["bf16_tflops"] * 1e12) * 1e3 / ms},
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": ach / peak, "traffic": None,
                      "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",

@@ -63,7 +63,12 @@ typedef struct tawpipe_dims {
   int32_t seq;           /* S, tokens per sequence fed to the model                              */
   int32_t micro_bs;      /* B, sequences per micro-batch                                          */
   int32_t dtype;         /* TAWPIPE_FP32 | TAWPIPE_BF16                                          */
-  int32_t ckpt;          /* 1: keep only each layer's input h_l, recompute in backward */
+  int32_t ckpt;          /* activation checkpointing: 0 none (all activations kept);
+                          * 1 keep each layer's input h_l and recompute the layer in backward, but
+                          * keep more of it while device memory allows (selective: attention O+LSE,
+                          * then q|k|v, then h1, then the MLP's gu and y, per (layer, micro-batch);
+                          * the recompute skips what was kept; results are bit-identical);
+                          * 2 keep h_l only (full recompute)                                      */
   int32_t schedule;      /* TAWPIPE_GWPS or TAWPIPE_RING, optionally | TAWPIPE_NO_CCO              */
   int32_t reserved;      /* must be 0                                                            */
   float lr, beta1, beta2, adam_eps, weight_decay;   /* AdamW, torch semantics (R1)               */
@@ -141,7 +146,8 @@ int tawpipe_ledger(uint64_t* out, int n);
  *  [6] GEMM launches                                 [7] attention ms   [8] attention GFLOP
  *  [9] AdamW ms   [10] AdamW algorithmic GB          [11] kernel launches in the step
  *  [12] peak device bytes allocated (GB)             [13] wire bytes per element
- *  [14] elementwise/norm ms                          [15] reserved                        LOCAL. */
+ *  [14] elementwise/norm ms
+ *  [15] algorithmic GFLOP of the recompute passes (checkpointing) executed in the step   LOCAL. */
 int tawpipe_stats(double* out, int n);
 
 /* Enable (1) / disable (0) per-kernel CUDA-event timing for tawpipe_stats.  LOCAL. */

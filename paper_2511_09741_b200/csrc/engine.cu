@@ -55,6 +55,21 @@ struct Acts {  // one (layer, micro-batch) forward's saved tensors
   float *r1, *lse, *r2;
 };
 
+// Selective checkpointing (ckpt = 1): beyond the residual checkpoint h_l, the step keeps, for as many
+// (layer, micro-batch) pairs as the device memory left after everything else allows, in this order:
+//   KEEP_ATTN  attention output O and LSE       (recompute skips the attention forward)
+//   KEEP_QKV   post-RoPE q|k|v                   (skips the QKV GEMM and RoPE)
+//   KEEP_H1    h1 = h + O·Woᵀ                    (skips the O GEMM)
+//   KEEP_MLP   gu = [x·Wgateᵀ | x·Wupᵀ] and y     (skips the gate/up GEMM + SwiGLU)
+// The two RMSNorms are always recomputed (cheap; their outputs and 1/rms feed the backward).  A kept tensor is
+// the output of the same kernel on the same inputs as its recompute would be: results are bit-identical.
+enum : uint8_t { KEEP_ATTN = 1, KEEP_QKV = 2, KEEP_H1 = 4, KEEP_MLP = 8 };
+struct Kept {
+  uint8_t flags = 0;
+  void *o = nullptr, *qkv = nullptr, *h1 = nullptr, *gu = nullptr, *y = nullptr;
+  float* lse = nullptr;
+};
+
 struct TimedRegion {
   cudaEvent_t a, b;
   int kind;  // 0 gemm, 1 attention, 2 adamw, 3 exposed wait, 4 elementwise, 5 weight comm, 6 grad comm
@@ -87,6 +102,8 @@ struct Ctx {
   // activations
   std::vector<void*> ck;  // (L+1) * m  residual-stream checkpoints h_l
   std::vector<Acts> acts;  // L*m (no ckpt) or 1 (ckpt)
+  std::vector<Kept> kept;  // L*m under ckpt == 1: activations kept beyond h_l (memory-budgeted)
+  double recompute_gflop = 0;  // algorithmic work of the recompute passes of the last step
   std::vector<void*> dhb;  // m: gradient of the residual stream per micro-batch
   void *dY = nullptr, *dGU = nullptr, *db = nullptr, *dh1 = nullptr, *dO = nullptr, *dqkv = nullptr, *da = nullptr;
   float *delta = nullptr, *dq_acc = nullptr;
@@ -462,38 +479,81 @@ LayerW layer_weights(void* W) {
 }
 
 Acts& acts_for(int l, int mb) { return g->dims.ckpt ? g->acts[0] : g->acts[static_cast<size_t>(l) * g->m + mb]; }
+// the activations of (l, mb) as the layer's forward / backward see them: kept tensors where selective
+// checkpointing kept them, else the scratch set (ckpt) or the per-layer set (no ckpt)
+struct View {
+  void *a, *qkv, *o, *h1, *b, *gu, *y;
+  float *r1, *lse, *r2;
+  uint8_t keep;
+};
+View view(int l, int mb) {
+  const Acts& A = acts_for(l, mb);
+  View v{A.a, A.qkv, A.o, A.h1, A.b, A.gu, A.y, A.r1, A.lse, A.r2, 0};
+  if (!g->kept.empty()) {
+    const Kept& k = g->kept[static_cast<size_t>(l) * g->m + mb];
+    v.keep = k.flags;
+    if (k.flags & KEEP_ATTN) {
+      v.o = k.o;
+      v.lse = k.lse;
+    }
+    if (k.flags & KEEP_QKV) v.qkv = k.qkv;
+    if (k.flags & KEEP_H1) v.h1 = k.h1;
+    if (k.flags & KEEP_MLP) {
+      v.gu = k.gu;
+      v.y = k.y;
+    }
+  }
+  return v;
+}
 void* ck(int l, int mb) { return g->ck[static_cast<size_t>(l) * g->m + mb]; }
 
 void layer_forward(int l, int mb, void* W, bool write_out) {
   cudaStream_t s = g->cs;
   const int64_t T = g->T, H = g->H, I = g->I;
   LayerW w = layer_weights(W);
-  Acts& A = acts_for(l, mb);
+  const View A = view(l, mb);
   void* hin = ck(l, mb);
+  // the recompute pass (write_out false) skips every step whose output selective checkpointing kept
+  const uint8_t skip = write_out ? 0 : A.keep;
+  double work = 0;
   k_rmsnorm_fwd(hin, w.attn_norm, A.a, A.r1, T, s);
-  gemm(T, 3 * H, H, A.a, H, true, w.wqkv, H, true, A.qkv, 3 * H, false, false, nullptr, s);
-  k_rope(A.qkv, false, s);
-  attn_fwd(A.qkv, A.o, A.lse, s);
-  gemm(T, H, H, A.o, H, true, w.wo, H, true, A.h1, H, false, false, hin, s);
+  if (!(skip & KEEP_QKV)) {
+    gemm(T, 3 * H, H, A.a, H, true, w.wqkv, H, true, A.qkv, 3 * H, false, false, nullptr, s);
+    k_rope(A.qkv, false, s);
+    work += 2.0 * T * 3 * H * H;
+  }
+  if (!(skip & KEEP_ATTN)) {
+    attn_fwd(A.qkv, A.o, A.lse, s);
+    work += attn_flops_fwd();
+  }
+  if (!(skip & KEEP_H1)) {
+    gemm(T, H, H, A.o, H, true, w.wo, H, true, A.h1, H, false, false, hin, s);
+    work += 2.0 * T * H * H;
+  }
   k_rmsnorm_fwd(A.h1, w.mlp_norm, A.b, A.r2, T, s);
-  if (g->bf && !gemm_force_simt()) {
-    // gate/up GEMM with the SwiGLU epilogue: y directly; gu is stored only when a backward will read it
-    // (no checkpointing, the recompute pass, or the last layer's last micro-batch which skips recompute)
-    const bool need_gu = !g->dims.ckpt || !write_out || (l == g->L - 1 && mb == g->m - 1);
-    GemmArgs a{T, 2 * I, H, A.b, H, true, w.wgu, H, true, need_gu ? A.gu : nullptr, 2 * I, false, false, nullptr};
-    a.epi = 3;
-    a.aux = A.y;
-    a.ldx = I;
-    a.I = I;
-    Timed t(s, 0, 2.0 * T * 2 * I * H);
-    gemm_tc_bf16(a, s);
-  } else {
-    gemm(T, 2 * I, H, A.b, H, true, w.wgu, H, true, A.gu, 2 * I, false, false, nullptr, s);
-    Timed t(s, 4, 0);
-    BY_TYPE(swiglu_fwd<float>((const float*)A.gu, (float*)A.y, T, (int)I, s),
-            swiglu_fwd<bf16>((const bf16*)A.gu, (bf16*)A.y, T, (int)I, s));
+  if (!(skip & KEEP_MLP)) {
+    work += 2.0 * T * 2 * I * H;
+    if (g->bf && !gemm_force_simt()) {
+      // gate/up GEMM with the SwiGLU epilogue: y directly; gu is stored only when a backward will read it
+      // (no checkpointing, the recompute pass, a kept MLP, or the last layer's last micro-batch which skips
+      // recompute)
+      const bool need_gu = !g->dims.ckpt || !write_out || (A.keep & KEEP_MLP) || (l == g->L - 1 && mb == g->m - 1);
+      GemmArgs a{T, 2 * I, H, A.b, H, true, w.wgu, H, true, need_gu ? A.gu : nullptr, 2 * I, false, false, nullptr};
+      a.epi = 3;
+      a.aux = A.y;
+      a.ldx = I;
+      a.I = I;
+      Timed t(s, 0, 2.0 * T * 2 * I * H);
+      gemm_tc_bf16(a, s);
+    } else {
+      gemm(T, 2 * I, H, A.b, H, true, w.wgu, H, true, A.gu, 2 * I, false, false, nullptr, s);
+      Timed t(s, 4, 0);
+      BY_TYPE(swiglu_fwd<float>((const float*)A.gu, (float*)A.y, T, (int)I, s),
+              swiglu_fwd<bf16>((const bf16*)A.gu, (bf16*)A.y, T, (int)I, s));
+    }
   }
   if (write_out) gemm(T, H, I, A.y, I, true, w.wdown, I, true, ck(l + 1, mb), H, false, false, A.h1, s);
+  if (!write_out) g->recompute_gflop += work * 1e-9;
 }
 
 void layer_backward(int l, int mb, void* W, float* G_) {
@@ -503,7 +563,7 @@ void layer_backward(int l, int mb, void* W, float* G_) {
   // recompute from the checkpoint h_l; the last layer's last micro-batch is still resident in the
   // scratch activations from the forward pass, so it needs no recompute
   if (g->dims.ckpt && !(l == g->L - 1 && mb == g->m - 1)) layer_forward(l, mb, W, false);
-  Acts& A = acts_for(l, mb);
+  const View A = view(l, mb);
   void* hin = ck(l, mb);
   void* dh = g->dhb[mb];
   float* gq = G_ + H;                      // Wq|Wk|Wv  [3H, H]
@@ -584,6 +644,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   c.step_t += 1;
   std::memset(c.ledger, 0, sizeof(c.ledger));
   c.regions.clear();
+  c.recompute_gflop = 0;
   c.ev_used = 0;
   c.launches_at_start = g_kstats.launches;
   const int64_t seqs = static_cast<int64_t>(c.m) * c.Bm;
@@ -726,6 +787,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   c.stats[11] = static_cast<double>(g_kstats.launches - c.launches_at_start);
   c.stats[12] = static_cast<double>(c.bytes_alloc) * 1e-9;
   c.stats[13] = static_cast<double>(c.esz);
+  c.stats[15] = c.recompute_gflop;
   return *c.h_loss / (static_cast<double>(c.N) * c.Bm * c.S);
 }
 
@@ -749,6 +811,7 @@ void validate(int P, int G, int L, const tawpipe_dims* d, int N, int world) {
   TP_CHECK((d->hidden / d->heads) % 2 == 0, TAWPIPE_ECONFIG, "d_h must be even (rotate-half RoPE)");
   TP_CHECK(d->dtype == TAWPIPE_FP32 || d->dtype == TAWPIPE_BF16, TAWPIPE_ECONFIG, "dtype must be FP32 or BF16");
   TP_CHECK(d->reserved == 0, TAWPIPE_ECONFIG, "reserved must be 0");
+  TP_CHECK(d->ckpt >= 0 && d->ckpt <= 2, TAWPIPE_ECONFIG, "ckpt must be 0, 1 or 2");
   TP_CHECK((d->schedule & ~(TAWPIPE_NO_CCO | TAWPIPE_RING)) == 0, TAWPIPE_ECONFIG, "unknown schedule flag");
   TP_CHECK(!(d->schedule & TAWPIPE_RING) || G == 1, TAWPIPE_ECONFIG,
            "TAWPIPE_RING owns whole layers per device: group_size must be 1");
@@ -946,6 +1009,32 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
     TP_CUDA(cudaMemcpyAsync(c.cosT, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c.cs));
     TP_CUDA(cudaMemcpyAsync(c.sinT, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c.cs));
     TP_CUDA(cudaStreamSynchronize(c.cs));
+  }
+  // ---- selective checkpointing (ckpt = 1): keep activations level by level while device memory allows
+  if (d->ckpt == 1) {
+    size_t fr = 0, tot = 0;
+    TP_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t margin = size_t(6) << 30;   // NCCL channels, allocator slack
+    size_t budget = fr > margin ? fr - margin : 0;
+    if (const char* e = std::getenv("TAWPIPE_KEEP_BUDGET_KB")) budget = std::min(budget, size_t(std::atoll(e)) << 10);
+    const size_t n = static_cast<size_t>(L) * m, TT = static_cast<size_t>(T);
+    const size_t cost[4] = {TT * H * esz + TT * c.nh * 4, TT * 3 * H * esz, TT * H * esz, TT * 3 * I * esz};
+    c.kept.assign(n, Kept{});
+    for (int lv = 0; lv < 4; ++lv) {
+      const size_t cnt = std::min(n, budget / cost[lv]);
+      for (size_t i = 0; i < cnt; ++i) {
+        Kept& k = c.kept[i];
+        switch (lv) {
+          case 0: k.o = dmalloc(TT * H * esz); k.lse = (float*)dmalloc(TT * c.nh * 4); break;
+          case 1: k.qkv = dmalloc(TT * 3 * H * esz); break;
+          case 2: k.h1 = dmalloc(TT * H * esz); break;
+          case 3: k.gu = dmalloc(TT * 2 * I * esz); k.y = dmalloc(TT * I * esz); break;
+        }
+        k.flags |= static_cast<uint8_t>(1u << lv);
+      }
+      budget -= cnt * cost[lv];
+      if (cnt < n) break;
+    }
   }
   // ---- seeded device-side initialisation of the owned stripes (R20)
   for (int l = 0; l < L + 2; ++l) {

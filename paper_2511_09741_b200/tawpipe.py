@@ -24,7 +24,7 @@ LEDGER_N, STATS_N = 24, 16
 
 STATS_NAMES = ("step_ms", "exposed_comm_ms", "weight_comm_ms", "grad_comm_ms", "gemm_ms", "gemm_gflop",
                "gemm_launches", "attn_ms", "attn_gflop", "adamw_ms", "adamw_gb", "kernel_launches",
-               "alloc_gb", "wire_bytes", "elementwise_ms", "reserved")
+               "alloc_gb", "wire_bytes", "elementwise_ms", "recompute_gflop")
 
 
 class TawpipeError(RuntimeError):

@@ -21,7 +21,13 @@ def T():
     return tawpipe
 
 
-def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=3, gains=True):
+def layer_fwd_flops(cfg, T_tok):
+    """(QKV, attention, O, gate/up) forward FLOPs of one layer on one micro-batch (App. B)."""
+    H, I, S = cfg.hidden, cfg.ffn, cfg.seq
+    return (2.0 * T_tok * 3 * H * H, 2.0 * H * (S + 1) * S * cfg.micro_bs, 2.0 * T_tok * H * H, 2.0 * T_tok * 2 * I * H)
+
+
+def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=3, gains=True, recompute=None):
     cfg = oracle_cfg(base)
     params = synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab)
     if gains:
@@ -37,6 +43,9 @@ def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=
         for step in range(steps):
             toks = synth.tokens(n_micro, cfg.micro_bs, cfg.seq, cfg.vocab, step=step)
             lg = sess.step(toks)
+            if recompute is not None:   # executed recompute work: which layers skipped what (selective ckpt)
+                got = sess.stats()["recompute_gflop"] * 1e9
+                assert abs(got - recompute) <= 1e-6 * max(recompute, 1.0), (got, recompute)
             lr, grads = om.train_step(st, toks, cfg)
             grads_all.append(grads)
             assert abs(lg - lr) / abs(lr) <= tol_loss, (step, lg, lr)
@@ -61,7 +70,25 @@ def test_c0_fp32_step_matches_oracle(T):
 
 
 def test_c0_fp32_ckpt_step_matches_oracle(T):
-    run_parity(T, C0, T.FP32, 1e-5, 1e-4, 1e-3, ckpt=1, steps=2)
+    # ckpt = 1 with memory to spare: every (layer, micro-batch) keeps O, q|k|v, h1 and the MLP: no recompute
+    run_parity(T, C0, T.FP32, 1e-5, 1e-4, 1e-3, ckpt=1, steps=2, recompute=0.0)
+
+
+def test_c0_fp32_full_recompute_step_matches_oracle(T):
+    cfg = oracle_cfg(C0)
+    n_rec = cfg.n_layers * 4 - 1               # every (layer, micro-batch) but the last layer's last one
+    run_parity(T, C0, T.FP32, 1e-5, 1e-4, 1e-3, ckpt=2, steps=2,
+               recompute=n_rec * sum(layer_fwd_flops(cfg, cfg.seq * cfg.micro_bs)))
+
+
+def test_c0_fp32_partial_keep_step_matches_oracle(T, monkeypatch):
+    # budget for O+LSE of all 8 (layer, micro-batch) pairs and q|k|v of the first 3 only (C0 fp32, T = 128):
+    # O+LSE 128·64·4 + 128·4·4 = 34816 B each, q|k|v 98304 B each -> 278528 + 3·98304 < 600 KiB < + 4·98304
+    cfg = oracle_cfg(C0)
+    monkeypatch.setenv("TAWPIPE_KEEP_BUDGET_KB", "600")
+    qkv, _, o, mlp = layer_fwd_flops(cfg, cfg.seq * cfg.micro_bs)
+    n_rec = cfg.n_layers * 4 - 1                # pairs 0..6 recomputed; 0..2 keep q|k|v, all keep O
+    run_parity(T, C0, T.FP32, 1e-5, 1e-4, 1e-3, ckpt=1, steps=2, recompute=n_rec * (o + mlp) + (n_rec - 3) * qkv)
 
 
 def test_c0b_bf16_step_matches_oracle(T):
@@ -70,4 +97,21 @@ def test_c0b_bf16_step_matches_oracle(T):
 
 def test_c0b_bf16_ckpt_microbs2_step_matches_oracle(T):
     base = dict(C0B, micro_bs=2)
-    run_parity(T, base, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=1, n_micro=2, steps=2)
+    run_parity(T, base, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=1, n_micro=2, steps=2, recompute=0.0)
+
+
+def test_c0b_bf16_full_recompute_step_matches_oracle(T):
+    cfg = oracle_cfg(C0B)
+    run_parity(T, C0B, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=2, n_micro=2, steps=2,
+               recompute=(cfg.n_layers * 2 - 1) * sum(layer_fwd_flops(cfg, cfg.seq * cfg.micro_bs)))
+
+
+def test_c0b_bf16_partial_keep_step_matches_oracle(T, monkeypatch):
+    # bf16 C0b (T = 256, H = 256, I = 768): O+LSE 256·256·2 + 256·2·4 = 133120 B, q|k|v 393216, h1 131072;
+    # budget 4·133120 + 4·393216 + 1·131072 = 2236416 B -> 2184 KiB: all O, all q|k|v, h1 of pair 0 only
+    cfg = oracle_cfg(C0B)
+    monkeypatch.setenv("TAWPIPE_KEEP_BUDGET_KB", "2200")
+    qkv, _, o, mlp = layer_fwd_flops(cfg, cfg.seq * cfg.micro_bs)
+    n_rec = cfg.n_layers * 2 - 1
+    run_parity(T, C0B, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=1, n_micro=2, steps=2,
+               recompute=n_rec * mlp + (n_rec - 1) * o)

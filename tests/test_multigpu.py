@@ -30,7 +30,7 @@ CASES = [
     ("c0b-2x2-bf16", C0B, 4, 2, 2, 4, 1, 1, False, False),
     ("c0b-1x2-bf16", C0B, 2, 2, 2, 2, 1, 0, False, False),
     ("c0-ring2", C0, 2, 1, 2, 4, 0, 0, False, True),          # NEXT-1 WeiPipe-style ring
-    ("c0-ring4", C0, 4, 1, 4, 4, 0, 1, False, True),
+    ("c0-ring4", C0, 4, 1, 4, 4, 0, 2, False, True),         # ckpt 2: full recompute
     ("c0b-ring4-bf16", C0B, 4, 1, 4, 4, 1, 0, False, True),
 ]
 

@@ -552,8 +552,9 @@ __global__ void __launch_bounds__(320, 1)
 // and consumed from TMEM as the A operand of O += P·V.  The softmax of tile j therefore never waits for the
 // P·V of tile j−1 except when the running max grows by more than 2^8 and O must be rescaled (lazy rescale):
 // the exp work overlaps P·V_{j−1} and S_{j+1} on the tensor core.
-//   warps 0-3: softmax, warp 4: TMA producer (Q once; K, V in 3-stage rings), warp 5: MMA issuer (the role warps
-//   have the highest warp ids on their SMSPs: hi-warp-id-first arbitration keeps the MMA issue off the softmax's tail)
+//   warps 0-3: softmax (thread = row), warp 4: S = Q·Kᵀ issuer, warp 5: P·V issuer, warp 6: TMA producer (Q once;
+//   K, V in 3-stage rings).  The MMA issuers run as whole warps (tcgen05.mma from one elected lane, descriptors in
+//   uniform registers) and sit on different SMSPs (see the kernel body).
 //   TMEM: S0 [0,128) S1 [128,256) O [384,512) (two S/P buffers in flight, see NSB)
 template <int DH>
 struct Fwd3Smem {
@@ -567,7 +568,7 @@ struct Fwd3Smem {
 };
 
 template <int DH, int EMU>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(224, 1)
     fa_fwd3_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
                    int nh, float scale2, unsigned long long* __restrict__ trace) {
   auto TR = [&](int it, int ev) {
@@ -584,8 +585,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
            *v_empty = bar + 1 + 3 * NST, *s_full = bar + 1 + 4 * NST, *p_ready = bar + 4 + 4 * NST,
-           *o_done = bar + 7 + 4 * NST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 4 * NST);
+           *o_done = bar + 7 + 4 * NST, *pv_done = bar + 8 + 4 * NST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10 + 4 * NST);
 
   const int n_q = S / BQ;
   // head-major order (the K/V of one head stay in L2 across its query tiles), heaviest tiles first in a head
@@ -607,21 +608,26 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < NSB; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_ready[i], 128);
+      mbar_init(&pv_done[i], 1);
     }
     mbar_init(o_done, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 4) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 384;   // S/P buffers at 0, 128, 256 (three tiles in flight)
+  const uint32_t tO = tmem + 384;   // S/P buffers at 0 and 128
 
-  if (warp == 4) {
+  // The two MMA chains are issued from different SMSPs: an SMSP that issues tcgen05.mma loses roughly the MMAs'
+  // execution time of issue slots (measured: the softmax warp sharing the issuer's SMSP finished each tile ~1000
+  // cycles late with both chains on one warp), so the S chain (warp 4, SMSP 0) and the P·V chain (warp 5,
+  // SMSP 1) each cost their neighbour half of that; the TMA producer is warp 6 (SMSP 2).
+  if (warp == 6) {
     if (lane == 0) {
       mbar_expect_tx(q_full, L::QB);
       for (int a = 0; a < DH / 64; ++a)
@@ -629,52 +635,52 @@ __global__ void __launch_bounds__(192, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int st = j % NST;
         const uint32_t ph = (j / NST) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_wait_sleep(&k_empty[st], ph ^ 1);
         mbar_expect_tx(&k_full[st], L::QB);
         for (int a = 0; a < DH / 64; ++a)
           tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
-        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_wait_sleep(&v_empty[st], ph ^ 1);
         mbar_expect_tx(&v_full[st], L::QB);
         for (int a = 0; a < DH / 64; ++a)
           tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
                       row0 + j * BQ);
       }
     }
+  } else if (warp == 4) {
+    // S chain: S_j = Q·K_jᵀ into buffer j % 2 once P·V_{j−2} (the previous reader of that buffer) completed
+    constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
+    const uint32_t sQ = smem_u32(sm + L::OFF_Q);
+    mbar_wait_sleep(q_full, 0);
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j % NST;
+      if (j >= NSB) mbar_wait_sleep(&pv_done[j % NSB], ((j - NSB) / NSB) & 1);
+      mbar_wait_sleep(&k_full[st], (j / NST) & 1);
+      tc_fence_after();
+      const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks)
+        umma_f16_w(tmem + (j % NSB) * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
+      umma_commit_w(&k_empty[st]);
+      umma_commit_w(&s_full[j % NSB]);
+    }
   } else if (warp == 5) {
-    if (lane == 0) {
-      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q);
-      auto issue_s = [&](int j) {
-        const int st = j % NST;
-        mbar_wait(&k_full[st], (j / NST) & 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
+    // P·V chain: O += P_j·V_j with P_j (bf16) read from TMEM as the A operand
+    constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j % NST;
+      mbar_wait_sleep(&p_ready[j % NSB], (j / NSB) & 1);
+      TR(j, 0);
+      mbar_wait_sleep(&v_full[st], (j / NST) & 1);
+      TR(j, 1);
+      tc_fence_after();
+      const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tmem + (j % NSB) * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
-        umma_commit(&k_empty[st]);
-        umma_commit(&s_full[j % NSB]);
-      };
-      mbar_wait(q_full, 0);
-      issue_s(0);
-      if (n_kv > 1) issue_s(1);
-      if (NSB > 2 && n_kv > 2) issue_s(2);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % NST;
-        mbar_wait(&p_ready[j % NSB], (j / NSB) & 1);
-        TR(j, 0);
-        mbar_wait(&v_full[st], (j / NST) & 1);
-        TR(j, 1);
-        tc_fence_after();
-        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks)
-          umma_f16_tmemA(tO, tmem + (j % NSB) * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
-        umma_commit(&v_empty[st]);
-        umma_commit(o_done);
-        if (j + NSB < n_kv) issue_s(j + NSB);   // overwrites S/P buffer (j % NSB) after P·V_j in issue order
-        TR(j, 2);
-      }
+      for (int ks = 0; ks < BQ / 16; ++ks)
+        umma_f16_tmemA_w(tO, tmem + (j % NSB) * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
+      umma_commit_w(&v_empty[st]);
+      umma_commit_w(&pv_done[j % NSB]);
+      umma_commit_w(o_done);
+      TR(j, 2);
     }
   } else {
     const int q = warp & 3;
@@ -756,7 +762,7 @@ __global__ void __launch_bounds__(192, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_ready[j % NSB]);
-      if (r == 0) TR(j, 4);
+      if (lane == 0) TR(j, 4 + q);   // per-warp p_done (slots 4..7)
     }
     mbar_wait(o_done, (n_kv - 1) & 1);
     tc_fence_after();
@@ -782,7 +788,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 4) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -1136,7 +1142,7 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
+    {  // whole warp (converged: descriptors stay uniform), one elected lane issues
       constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
       constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
       constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
@@ -1148,8 +1154,10 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
         const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
-        umma_commit(s_full);
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          umma_f16_w(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
+        }
+        umma_commit_w(s_full);
         TR(it, 0);
       };
       mbar_wait(kv_full, 0);
@@ -1162,14 +1170,14 @@ __global__ void __launch_bounds__(320, 1)
         TR(it, 1);
         tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
-        umma_commit(dp_full);
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
+        umma_commit_w(dp_full);
         mbar_wait(p_ready, it & 1);
         TR(it, 2);
         tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
-        umma_commit(do_empty);
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA_w(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
+        umma_commit_w(do_empty);
         mbar_wait(ds_ready, it & 1);
         TR(it, 3);
         // Pᵀ_it fully consumed (dV issued before, dS pass done): Sᵀ_{it+1} goes first so that the softmax warps
@@ -1177,11 +1185,11 @@ __global__ void __launch_bounds__(320, 1)
         if (it + 1 < n_it) issue_s(it + 1);
         tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
-        umma_commit(&q_empty[st]);
-        umma_commit(mm2_done);
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
+        umma_commit_w(&q_empty[st]);
+        umma_commit_w(mm2_done);
       }
     }
   } else if (warp < 4) {
@@ -1272,6 +1280,7 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       mbar_arrive(ds_ready);
       if (t == 0) TR(it, 8);
+      if (lane == 0) TR(it, 12 + warp);   // per-warp dS done
     }
     // dK (× softmax scale) and dV rows of this key tile
     mbar_wait(mm2_done, (n_it - 1) & 1);
@@ -1442,7 +1451,7 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
   do {                                                                                                 \
     static bool once = (prep(fa_fwd3_kernel<D, E>, Fwd3Smem<D>::BYTES), true);                        \
     (void)once;                                                                                        \
-    fa_fwd3_kernel<D, E><<<grid3, 192, Fwd3Smem<D>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);   \
+    fa_fwd3_kernel<D, E><<<grid3, 224, Fwd3Smem<D>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);   \
   } while (0)
     if (dh == 128) {
       if (emu == 1) FWD3_LAUNCH(128, 1);
@@ -1461,9 +1470,10 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
       TP_CUDA(cudaMemcpy(hbuf, ftrace, sizeof(hbuf), cudaMemcpyDeviceToHost));
       const unsigned long long t0 = hbuf[3];
       for (int it = 0; it < 12; ++it)
-        std::fprintf(stderr, "fwd j %2d: mma:p_ready=%lld mma:v_full=%lld mma:issued=%lld smx:s_full=%lld smx:p_done=%lld\n", it,
+        std::fprintf(stderr, "fwd j %2d: mma:p_ready=%lld mma:v_full=%lld mma:issued=%lld smx:s_full=%lld smx:p_done w0..3=%lld %lld %lld %lld\n", it,
                      (long long)(hbuf[it * 16] - t0), (long long)(hbuf[it * 16 + 1] - t0), (long long)(hbuf[it * 16 + 2] - t0),
-                     (long long)(hbuf[it * 16 + 3] - t0), (long long)(hbuf[it * 16 + 4] - t0));
+                     (long long)(hbuf[it * 16 + 3] - t0), (long long)(hbuf[it * 16 + 4] - t0), (long long)(hbuf[it * 16 + 5] - t0),
+                     (long long)(hbuf[it * 16 + 6] - t0), (long long)(hbuf[it * 16 + 7] - t0));
     }
     return;
   }
@@ -1554,13 +1564,13 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   if (trace) {
     unsigned long long h[32 * 16];
     TP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
-    static const char* names[12] = {"mma:S_issued", "mma:dO+tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
+    static const char* names[16] = {"mma:S_issued", "mma:dO+tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
                                     "cmp:p_done", "cmp:dp_full", "cmp:mm2_prev", "cmp:ds_done", "dq:mm2_done",
-                                    "dq:tdp_free", "dq:staged"};
+                                    "dq:tdp_free", "dq:staged", "cmp:ds_w0", "cmp:ds_w1", "cmp:ds_w2", "cmp:ds_w3"};
     const unsigned long long t0 = h[0];
     for (int it = 0; it < 12; ++it) {
       std::fprintf(stderr, "it %2d:", it);
-      for (int e = 0; e < 12; ++e) std::fprintf(stderr, " %s=%lld", names[e], (long long)(h[it * 16 + e] - t0));
+      for (int e = 0; e < 16; ++e) std::fprintf(stderr, " %s=%lld", names[e], (long long)(h[it * 16 + e] - t0));
       std::fprintf(stderr, "\n");
     }
   }

@@ -195,6 +195,9 @@ def run_ours(args, c):
     t_init = time.time()
     sess = T.Session(world, G, dims, N)
     sess.set_timing(True)
+    emu_node = args.emu_node_size or G
+    if args.emu_inter_gbps > 0:
+        sess.set_link_emulation(args.emu_inter_gbps, args.emu_latency_us, emu_node)
     if verbose:
         print(f"[rank {rank}] init {time.time() - t_init:.1f} s, {sess.stats()['alloc_gb']:.1f} GB", file=sys.stderr,
               flush=True)
@@ -241,6 +244,10 @@ def run_ours(args, c):
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    trace = sess.trace()
+    if args.trace and rank == 0:
+        with open(args.trace, "w") as fh:
+            json.dump(trace, fh)
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / n_e2e)
     tokens_step = N * c["B"] * c["S"]
     st = {k: statistics.mean(s[k] for s in stats_acc) for k in stats_acc[0]}
@@ -279,11 +286,14 @@ def run_ours(args, c):
                    "seq_len": c["S"], "parallelism": f"tawpipe {world // G}x{G} (D x G)",
                    "l2": "inputs and weights far larger than L2 (no flush needed)",
                    "schedule": "no-CCO ablation" if args.no_cco else "GWPS+DBS+CCO",
+                   **({"link_emulation": {"inter_gbps": args.emu_inter_gbps, "latency_us": args.emu_latency_us,
+                                          "node_size": emu_node}} if args.emu_inter_gbps > 0 else {}),
                    "checkpointing": (f"selective: residual stream + kept activations while memory allows; "
                                      f"recompute executed {rec_gflop / 1e3:.1f} TFLOP of "
                                      f"{(flops_per_token(c) - flops_per_token(c, recompute=False)) * c['m'] * c['B'] * c['S'] / 1e12:.1f}")
                                     if c["ckpt"] else "none"},
         "exposed_comm_ms": exposed, "exposed_comm_frac": exposed / ms, "comm": comm,
+        "compute_idle_frac": max_over_ranks(trace.get("otherData", {}).get("compute_idle_frac", 0.0)),
         "step_roofline_frac": step_roof_ms / ms,
         # SURVEY.md §8(d) conventions: the step roofline on the executed work (above), on model FLOPs only (MFU,
         # no recompute) and on model FLOPs + a full checkpoint recompute (the survey table's HFU figure)
@@ -315,6 +325,8 @@ def run_ours(args, c):
             db = T.ModelDims(**{**dims.__dict__, "schedule": sched})
             sb = T.Session(world, Gb, db, N)
             sb.set_timing(True)
+            if args.emu_inter_gbps > 0:   # same emulated nodes (physical placement), whatever the schedule's groups
+                sb.set_link_emulation(args.emu_inter_gbps, args.emu_latency_us, emu_node)
             for i in range(max(1, min(args.warmup, 2))):
                 sb.step_device(tok_dev[i % 2].data_ptr())
             barrier()
@@ -354,6 +366,11 @@ def main():
     ap.add_argument("--no-cco", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true", help="skip the in-library FSDP / ring comparison runs")
+    ap.add_argument("--emu-inter-gbps", type=float, default=0.0,
+                    help="NEXT-3: pace transfers across emulated nodes to this GB/s (paper testbed: 1.25)")
+    ap.add_argument("--emu-latency-us", type=float, default=30.0)
+    ap.add_argument("--emu-node-size", type=int, default=0, help="devices per emulated node (0: the group size)")
+    ap.add_argument("--trace", default="", help="NEXT-4: write rank 0's Trace-Event JSON of the last timed step")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     if args.impl == "reference":

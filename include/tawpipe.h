@@ -153,6 +153,25 @@ int tawpipe_stats(double* out, int n);
 /* Enable (1) / disable (0) per-kernel CUDA-event timing for tawpipe_stats.  LOCAL. */
 int tawpipe_set_timing(int on);
 
+/* Trace-Event JSON (chrome://tracing / Perfetto) of the last step run with timing on (NEXT-4):
+ * "X" events {name: gemm | attention | adamw | exposed_comm_wait | elementwise | weight_comm | grad_comm,
+ * ts/dur in µs from the step's first compute-stream event, pid = rank, tid = stream (0 compute, 1 weights,
+ * 2 gradients), args.work = algorithmic FLOP or bytes}; otherData = {rank, step, step_ms, busy_ms[3] (union of
+ * each stream's regions), exposed_comm_ms, compute_idle_frac (compute stream neither computing nor waiting on
+ * communication)}.  Writes min(length, cap − 1) bytes plus a NUL to `out` (caller-owned; may be NULL to query the
+ * size) and returns the full length (0 before a timed step), or < 0 on error.  LOCAL. */
+int64_t tawpipe_trace_json(char* out, int64_t cap);
+
+/* Emulated link hierarchy (NEXT-3): devices are grouped into emulated nodes of `node_size`
+ * consecutive ranks (0: the schedule's group size G).  Every weight / gradient transfer that crosses a node
+ * boundary is followed on each participating stream by a device-side delay of latency_us + bytes / inter_gbps
+ * (bytes: what the busiest endpoint moves across the boundary in that exchange: (D−1) stripes for the rail
+ * exchange, (G−1) stripes for a cross-node ring all-gather / reduce-scatter, one unit per ring hop).  The paper's
+ * testbed: 1.25 GB/s and 30 µs across nodes.  inter_gbps = 0 disables.  Results and the
+ * ledger are unchanged.  Applies to later steps.  LOCAL (set the same values on every rank).  Returns 0 or
+ * TAWPIPE_ECONFIG (negative values, node_size not dividing n_devices). */
+int tawpipe_set_link_emulation(double inter_gbps, double latency_us, int node_size);
+
 /* Thread-local description of the last error (never NULL).  LOCAL. */
 const char* tawpipe_last_error(void);
 

@@ -117,6 +117,8 @@ void add_cast(const T* a, const float* b, T* y, int64_t n, cudaStream_t s);
 template <typename T>
 void init_normal(T* wire, float* master, int64_t n, int64_t global_off, uint64_t seed, float std, cudaStream_t s);
 void fill_f32(float* x, int64_t n, float v, cudaStream_t s);
+// emulated link time: one thread spins on the global timer for `seconds` on stream s (NEXT-3)
+void link_delay(double seconds, cudaStream_t s);
 
 struct AdamParams {
   float lr, beta1, beta2, eps, wd;

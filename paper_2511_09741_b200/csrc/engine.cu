@@ -12,6 +12,8 @@
 // Every step of the path runs in this library's kernels; torch only bootstraps the process group (no CPU fallback).
 #include <nccl.h>
 
+#include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -74,6 +76,7 @@ struct TimedRegion {
   cudaEvent_t a, b;
   int kind;  // 0 gemm, 1 attention, 2 adamw, 3 exposed wait, 4 elementwise, 5 weight comm, 6 grad comm
   double work;
+  int stream;  // 0 compute, 1 weights, 2 gradients
 };
 
 struct Ctx {
@@ -104,6 +107,10 @@ struct Ctx {
   std::vector<Acts> acts;  // L*m (no ckpt) or 1 (ckpt)
   std::vector<Kept> kept;  // L*m under ckpt == 1: activations kept beyond h_l (memory-budgeted)
   double recompute_gflop = 0;  // algorithmic work of the recompute passes of the last step
+  std::string trace_json;      // Trace-Event JSON of the last timed step (NEXT-4)
+  // emulated link hierarchy (NEXT-3): transfers that cross an emulated node boundary are paced
+  double emu_gbps = 0, emu_lat_us = 0;
+  int emu_node = 0;            // devices per emulated node (0: the schedule's group size G)
   std::vector<void*> dhb;  // m: gradient of the residual stream per micro-batch
   void *dY = nullptr, *dGU = nullptr, *db = nullptr, *dh1 = nullptr, *dO = nullptr, *dqkv = nullptr, *da = nullptr;
   float *delta = nullptr, *dq_acc = nullptr;
@@ -177,6 +184,7 @@ struct Timed {  // RAII CUDA-event bracket on a stream (only when timing is enab
     r.b = pool_event();
     r.kind = kind;
     r.work = work;
+    r.stream = st == g->cs ? 0 : st == g->ws ? 1 : 2;
     TP_CUDA(cudaEventRecord(r.a, s));
   }
   ~Timed() noexcept(false) {
@@ -192,6 +200,22 @@ struct Timed {  // RAII CUDA-event bracket on a stream (only when timing is enab
 
 inline ncclDataType_t wire_type() { return g->bf ? ncclBfloat16 : ncclFloat32; }
 inline char* wptr(void* base, int64_t elems) { return static_cast<char*>(base) + elems * static_cast<int64_t>(g->esz); }
+
+// ------------------------------------------------------------------------------------ link emulation (NEXT-3)
+// With tawpipe_set_link_emulation on, a transfer whose endpoints lie in different emulated nodes (node of device d
+// = d / node_size) is followed, on every participating stream, by a device-side delay of latency + bytes / bandwidth,
+// where bytes is what the busiest endpoint moves across the node boundary in that exchange (alpha-beta model,
+// SPEC.md:85 "a800-10gbe": 1.25 GB/s, 30 µs).  The data and the ledger are unchanged; only time is added.
+int emu_node_size() { return g->emu_node > 0 ? g->emu_node : g->G; }
+bool emu_crosses(int a, int b) { return g->emu_gbps > 0 && a / emu_node_size() != b / emu_node_size(); }
+void emu_delay(double bytes, cudaStream_t s) {
+  if (g->emu_gbps <= 0) return;
+  link_delay(g->emu_lat_us * 1e-6 + bytes / (g->emu_gbps * 1e9), s);
+}
+// rail exchange among the D devices (kk·G + j): crosses nodes iff the rail spans more than one emulated node
+bool emu_rail_crosses() { return g->D > 1 && emu_crosses(g->j, (g->D - 1) * g->G + g->j); }
+// group collective among devices k·G .. k·G + G − 1
+bool emu_group_crosses() { return g->G > 1 && emu_crosses(g->k * g->G, g->k * g->G + g->G - 1); }
 
 // ------------------------------------------------------------------------------------ kernel dispatch
 bool gemm_force_simt() {
@@ -335,8 +359,14 @@ void gather(int uid, void* dst) {
   if (g->ring) {  // owner -> owner+1 -> ... : receive from d-1, then forward to d+1 (stream-ordered)
     const int d = g->rank, P = g->P;
     void* buf = u.owned ? own : dst;
-    if (!u.owned) TP_NCCL(ncclRecv(buf, u.n_pad, wire_type(), (d + P - 1) % P, g->wr, g->ws));
-    if ((d + 1) % P != u.owner) TP_NCCL(ncclSend(buf, u.n_pad, wire_type(), (d + 1) % P, g->wr, g->ws));
+    if (!u.owned) {
+      TP_NCCL(ncclRecv(buf, u.n_pad, wire_type(), (d + P - 1) % P, g->wr, g->ws));
+      if (emu_crosses((d + P - 1) % P, d)) emu_delay(static_cast<double>(u.n_pad) * g->esz, g->ws);
+    }
+    if ((d + 1) % P != u.owner) {
+      TP_NCCL(ncclSend(buf, u.n_pad, wire_type(), (d + 1) % P, g->wr, g->ws));
+      if (emu_crosses(d, (d + 1) % P)) emu_delay(static_cast<double>(u.n_pad) * g->esz, g->ws);
+    }
     ledger_gather_ring(u, d, P, g->ledger);
     return;
   }
@@ -349,10 +379,14 @@ void gather(int uid, void* dst) {
       TP_NCCL(ncclRecv(wptr(dst, g->j * u.s), u.s, wire_type(), u.owner, g->wr, g->ws));
     }
     TP_NCCL(ncclGroupEnd());
+    // the owner's link carries its stripe to each of the D − 1 other groups
+    if (emu_rail_crosses()) emu_delay(static_cast<double>(g->D - 1) * u.s * g->esz, g->ws);
   }
   if (g->G > 1) {
     const void* send = u.owned ? own : wptr(dst, g->j * u.s);
     TP_NCCL(ncclAllGather(send, dst, u.s, wire_type(), g->wg, g->ws));
+    // ring all-gather: each link across the node boundary carries G − 1 stripes
+    if (emu_group_crosses()) emu_delay(static_cast<double>(g->G - 1) * u.s * g->esz, g->ws);
   }
   ledger_gather(u, g->G, g->D, g->ledger);
 }
@@ -375,6 +409,7 @@ void reduce_ring(const Unit& u, float* gacc) {
   if (!first) {
     Timed t(s, 6, 0);
     TP_NCCL(ncclRecv(g->crecv, u.n_pad, wire_type(), prev, g->gr, s));
+    if (emu_crosses(prev, d)) emu_delay(static_cast<double>(u.n_pad) * g->esz, s);
   }
   if (u.owned) {
     const void* contrib[2] = {gacc, g->crecv};
@@ -390,6 +425,7 @@ void reduce_ring(const Unit& u, float* gacc) {
     }
     Timed t(s, 6, 0);
     TP_NCCL(ncclSend(g->gwire, u.n_pad, wire_type(), next, g->gr, s));
+    if (emu_crosses(d, next)) emu_delay(static_cast<double>(u.n_pad) * g->esz, s);
   }
   ledger_reduce_ring(u, d, P, g->ledger);
 }
@@ -412,6 +448,7 @@ void reduce_and_update(int uid, float* gacc) {
   if (g->G > 1) {
     Timed t(s, 6, 0);
     TP_NCCL(ncclReduceScatter(g->gwire, g->rsout, u.s, wire_type(), ncclSum, g->gg, s));
+    if (emu_group_crosses()) emu_delay(static_cast<double>(g->G - 1) * u.s * g->esz, s);
     own_partial = g->rsout;
   }
   if (g->D > 1) {
@@ -425,6 +462,8 @@ void reduce_and_update(int uid, float* gacc) {
       TP_NCCL(ncclSend(own_partial, u.s, wire_type(), u.owner, g->gr, s));
     }
     TP_NCCL(ncclGroupEnd());
+    // the owner's link receives the D − 1 group partials
+    if (emu_rail_crosses()) emu_delay(static_cast<double>(g->D - 1) * u.s * g->esz, s);
   }
   ledger_reduce(u, g->G, g->D, g->ledger);
   if (!u.owned) return;
@@ -638,6 +677,58 @@ __global__ void split_tokens_kernel(const int32_t* __restrict__ tok, int64_t seq
   }
 }
 
+// ------------------------------------------------------------------------------------ trace export (NEXT-4)
+// Trace-Event JSON ("X" complete events, microseconds from the step's first compute-stream event) of the last
+// timed step: one thread per stream (0 compute, 1 weights, 2 gradients), pid = rank.  otherData carries the
+// step time and, per stream, the busy time (union of its regions) and the compute stream's idle ("bubble")
+// fraction: time the compute stream is neither running a timed kernel nor waiting on communication.
+void build_trace_json(float step_ms) {
+  Ctx& c = *g;
+  static const char* kind_name[7] = {"gemm", "attention", "adamw", "exposed_comm_wait", "elementwise",
+                                     "weight_comm", "grad_comm"};
+  std::vector<std::array<double, 2>> iv[3];
+  std::string out;
+  out.reserve(c.regions.size() * 128 + 512);
+  out += "{\"traceEvents\":[";
+  char buf[256];
+  bool first = true;
+  for (auto& r : c.regions) {
+    float t0 = 0.f, t1 = 0.f;
+    TP_CUDA(cudaEventElapsedTime(&t0, c.ev_s0, r.a));
+    TP_CUDA(cudaEventElapsedTime(&t1, c.ev_s0, r.b));
+    if (r.kind != 3) iv[r.stream].push_back({static_cast<double>(t0), static_cast<double>(t1)});
+    std::snprintf(buf, sizeof(buf),
+                  "%s{\"name\":\"%s\",\"cat\":\"tawpipe\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%d,"
+                  "\"tid\":%d,\"args\":{\"work\":%.6g}}",
+                  first ? "" : ",", kind_name[r.kind], t0 * 1e3, (t1 - t0) * 1e3, c.rank, r.stream, r.work);
+    out += buf;
+    first = false;
+  }
+  double busy[3] = {0, 0, 0};
+  for (int st = 0; st < 3; ++st) {  // union of intervals
+    auto& v = iv[st];
+    std::sort(v.begin(), v.end());
+    double cur0 = -1, cur1 = -1;
+    for (auto& x : v) {
+      if (x[0] > cur1) {
+        if (cur1 > cur0) busy[st] += cur1 - cur0;
+        cur0 = x[0];
+        cur1 = x[1];
+      } else if (x[1] > cur1) {
+        cur1 = x[1];
+      }
+    }
+    if (cur1 > cur0) busy[st] += cur1 - cur0;
+  }
+  std::snprintf(buf, sizeof(buf),
+                "],\"displayTimeUnit\":\"ms\",\"otherData\":{\"rank\":%d,\"step\":%d,\"step_ms\":%.4f,"
+                "\"busy_ms\":[%.4f,%.4f,%.4f],\"exposed_comm_ms\":%.4f,\"compute_idle_frac\":%.6f}}",
+                c.rank, c.step_t, step_ms, busy[0], busy[1], busy[2], c.stats[1],
+                step_ms > 0 ? std::max(0.0, 1.0 - (busy[0] + c.stats[1]) / step_ms) : 0.0);
+  out += buf;
+  c.trace_json.swap(out);
+}
+
 // ------------------------------------------------------------------------------------ one iteration
 double run_step(const int32_t* tokens, bool device_tokens) {
   Ctx& c = *g;
@@ -788,6 +879,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   c.stats[12] = static_cast<double>(c.bytes_alloc) * 1e-9;
   c.stats[13] = static_cast<double>(c.esz);
   c.stats[15] = c.recompute_gflop;
+  if (c.timing) build_trace_json(ms);
   return *c.h_loss / (static_cast<double>(c.N) * c.Bm * c.S);
 }
 
@@ -1274,6 +1366,35 @@ int tawpipe_set_timing(int on) {
     return TAWPIPE_EUNINIT;
   }
   g->timing = on != 0;
+  return TAWPIPE_OK;
+}
+
+int64_t tawpipe_trace_json(char* out, int64_t cap) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  const int64_t n = static_cast<int64_t>(g->trace_json.size());
+  if (out != nullptr && cap > 0) {
+    const int64_t k = std::min<int64_t>(n, cap - 1);
+    std::memcpy(out, g->trace_json.data(), static_cast<size_t>(k));
+    out[k] = 0;
+  }
+  return n;
+}
+
+int tawpipe_set_link_emulation(double inter_gbps, double latency_us, int node_size) {
+  if (!g || !g->inited) {
+    g_err = "not initialised";
+    return TAWPIPE_EUNINIT;
+  }
+  if (!(inter_gbps >= 0) || !(latency_us >= 0) || node_size < 0 || (node_size > 0 && g->P % node_size != 0)) {
+    g_err = "link emulation: need inter_gbps >= 0, latency_us >= 0, node_size >= 0 dividing n_devices";
+    return TAWPIPE_ECONFIG;
+  }
+  g->emu_gbps = inter_gbps;
+  g->emu_lat_us = latency_us;
+  g->emu_node = node_size;
   return TAWPIPE_OK;
 }
 

@@ -688,4 +688,21 @@ void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_
 INST(float)
 INST(bf16)
 
+// ------------------------------------------------------------------------------------ emulated link delay
+__global__ void link_delay_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+void link_delay(double seconds, cudaStream_t s) {
+  if (!(seconds > 0)) return;
+  link_delay_kernel<<<1, 32, 0, s>>>(static_cast<unsigned long long>(seconds * 1e9));
+  TP_CUDA(cudaGetLastError());
+  g_kstats.launches++;
+}
+
 }  // namespace tp

@@ -69,6 +69,8 @@ def lib():
         "tawpipe_ledger": (i32, [vp, i32]),
         "tawpipe_stats": (i32, [vp, i32]),
         "tawpipe_set_timing": (i32, [i32]),
+        "tawpipe_trace_json": (i64, [vp, i64]),
+        "tawpipe_set_link_emulation": (i32, [ctypes.c_double, ctypes.c_double, i32]),
         "tawpipe_last_error": (ctypes.c_char_p, []),
         "tawpipe_finalize": (None, []),
         "tawpipe_gemm": (i32, [i32, i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, vp, vp]),
@@ -225,6 +227,22 @@ class Session:
 
     def set_timing(self, on: bool):
         _check(lib().tawpipe_set_timing(1 if on else 0))
+
+    def trace(self) -> dict:
+        """Trace-Event JSON of the last timed step (tawpipe_trace_json), parsed; {} before any timed step."""
+        n = lib().tawpipe_trace_json(None, 0)
+        if n < 0:
+            _check(int(n))
+        if n == 0:
+            return {}
+        buf = ctypes.create_string_buffer(int(n) + 1)
+        lib().tawpipe_trace_json(buf, n + 1)
+        import json
+        return json.loads(buf.value.decode())
+
+    def set_link_emulation(self, inter_gbps: float, latency_us: float = 0.0, node_size: int = 0):
+        """Pace transfers that cross emulated node boundaries (tawpipe_set_link_emulation); 0 GB/s disables."""
+        _check(lib().tawpipe_set_link_emulation(float(inter_gbps), float(latency_us), int(node_size)))
 
     def close(self):
         lib().tawpipe_finalize()

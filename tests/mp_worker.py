@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--ckpt", type=int, default=0)
     ap.add_argument("--no-cco", action="store_true")
     ap.add_argument("--ring", action="store_true")
+    ap.add_argument("--emu-gbps", type=float, default=0.0)   # NEXT-3 emulated inter-node link
+    ap.add_argument("--emu-node", type=int, default=0)
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     cfg = oracle_cfg(json.loads(a.cfg))
@@ -36,13 +38,18 @@ def main():
                        schedule=(T.NO_CCO if a.no_cco else T.GWPS) | (T.RING if a.ring else 0))
     sess = T.Session(world, a.G, dims, a.N)
     sess.load(T.pack_full_model(params))
-    losses, ledgers = [], []
+    if a.emu_gbps > 0:
+        sess.set_link_emulation(a.emu_gbps, 30.0, a.emu_node)
+        sess.set_timing(True)
+    losses, ledgers, comm_ms = [], [], []
     for step in range(a.steps):
         toks = synth.tokens(a.N, cfg.micro_bs, cfg.seq, cfg.vocab, step=step)
         losses.append(sess.step(toks))
         ledgers.append(sess.ledger())
+        stt = sess.stats()
+        comm_ms.append(stt["weight_comm_ms"] + stt["grad_comm_ms"])
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), losses=np.array(losses), ledgers=np.array(ledgers, np.uint64),
-             shard=sess.shard())
+             shard=sess.shard(), comm_ms=np.array(comm_ms))
     sess.close()
 
 

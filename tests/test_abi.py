@@ -39,6 +39,8 @@ def test_errors_before_init(L):
     assert L.tawpipe_shard_elems() == T.EUNINIT
     import math
     assert math.isnan(L.tawpipe_step(None))
+    assert L.tawpipe_trace_json(None, 0) == T.EUNINIT
+    assert L.tawpipe_set_link_emulation(1.25, 30.0, 2) == T.EUNINIT
 
 
 def test_unique_id_without_gpu(L):

@@ -115,3 +115,33 @@ def test_c0b_bf16_partial_keep_step_matches_oracle(T, monkeypatch):
     n_rec = cfg.n_layers * 2 - 1
     run_parity(T, C0B, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=1, n_micro=2, steps=2,
                recompute=n_rec * mlp + (n_rec - 1) * o)
+
+
+def test_trace_export_and_idle_fraction(T):
+    """NEXT-4: the Trace-Event JSON of a timed step is well formed and consistent with the step's own timing."""
+    cfg = oracle_cfg(C0B)
+    dims = T.ModelDims(n_layers=cfg.n_layers, hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, vocab=cfg.vocab,
+                       seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=T.BF16, ckpt=1)
+    sess = T.Session(1, 1, dims, 2)
+    try:
+        assert sess.trace() == {}                      # nothing timed yet
+        sess.set_timing(True)
+        sess.set_link_emulation(1.25, 30.0, 0)         # P = 1: nothing crosses a node, nothing changes
+        sess.step(synth.tokens(2, cfg.micro_bs, cfg.seq, cfg.vocab, step=0))
+        st, tr = sess.stats(), sess.trace()
+        ev, od = tr["traceEvents"], tr["otherData"]
+        names = {"gemm", "attention", "adamw", "exposed_comm_wait", "elementwise", "weight_comm", "grad_comm"}
+        assert ev and all(e["ph"] == "X" and e["name"] in names and e["tid"] in (0, 1, 2) for e in ev)
+        step_us = st["step_ms"] * 1e3
+        assert all(-1.0 <= e["ts"] and e["ts"] + e["dur"] <= step_us + 1.0 for e in ev)
+        assert abs(od["step_ms"] - st["step_ms"]) < 1e-3
+        n_gemm = sum(1 for e in ev if e["name"] == "gemm")
+        assert n_gemm == st["gemm_launches"]
+        gemm_ms = sum(e["dur"] for e in ev if e["name"] == "gemm") / 1e3
+        assert abs(gemm_ms - st["gemm_ms"]) <= 1e-3 * max(1.0, st["gemm_ms"])
+        assert 0.0 <= od["compute_idle_frac"] <= 1.0 and od["busy_ms"][0] <= st["step_ms"] + 1e-3
+        with pytest.raises(T.TawpipeError):
+            sess.set_link_emulation(-1.0, 0.0, 0)
+    finally:
+        sess.close()
+        T.bootstrap(0, 1, 0)

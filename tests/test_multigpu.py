@@ -19,7 +19,7 @@ from oracle import ledger as LG
 torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
-# (name, base dims, P, G, L, N, dtype, ckpt, no_cco, ring)
+# (name, base dims, P, G, L, N, dtype, ckpt, no_cco, ring[, emulated inter-node GB/s, emulated node size])
 CASES = [
     ("c0-1x2-fsdp", C0, 2, 2, 2, 4, 0, 0, False, False),
     ("c0-2x1-p2p", C0, 2, 1, 2, 4, 0, 0, False, False),
@@ -32,7 +32,11 @@ CASES = [
     ("c0-ring2", C0, 2, 1, 2, 4, 0, 0, False, True),          # NEXT-1 WeiPipe-style ring
     ("c0-ring4", C0, 4, 1, 4, 4, 0, 2, False, True),         # ckpt 2: full recompute
     ("c0b-ring4-bf16", C0B, 4, 1, 4, 4, 1, 0, False, True),
+    # NEXT-3: 2 emulated nodes of 2 at 0.05 GB/s: same results and ledger, paced rail traffic
+    ("c0-2x2-emu", C0, 4, 2, 2, 4, 0, 0, False, False, 0.05, 2),
+    ("c0-ring4-emu", C0, 4, 1, 4, 4, 0, 0, False, True, 0.05, 2),
 ]
+CASES = [c if len(c) == 12 else c + (0.0, 0) for c in CASES]
 
 
 def free_port():
@@ -41,8 +45,9 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco,ring", CASES, ids=[c[0] for c in CASES])
-def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco, ring):
+@pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco,ring,emu_gbps,emu_node", CASES,
+                         ids=[c[0] for c in CASES])
+def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco, ring, emu_gbps, emu_node):
     if not torch.cuda.is_available() or torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     cfg = oracle_cfg(base, n_layers=L)
@@ -51,7 +56,7 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--cfg", json.dumps(dict(base, n_layers=L)), "--G", str(G), "--N", str(N), "--steps", str(steps),
            "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else []) \
-        + (["--ring"] if ring else [])
+        + (["--ring"] if ring else []) + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
@@ -79,3 +84,12 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
         expect = LG.ring_ledger(L, P, i, s, e, f, r=1) if ring else LG.closed_form(L, P, G, i // G, s, e, f, r=1)
         for step in range(steps):
             assert [int(x) for x in res[i]["ledgers"][step]] == expect, (i, step)
+    if emu_gbps and not ring:
+        # NEXT-3 pacing: every rail exchange (D > 1, groups = emulated nodes) adds 30 µs + (D−1)·stripe bytes / bw
+        # to each participant's comm stream: gathers E, L blocks, F and L−1 re-gathers; reductions F, L blocks, E
+        D, esz = P // G, (4 if dtype == 0 else 2)
+        units = [e] + [s] * L + [f] + [s] * (L - 1) + [f] + [s] * L + [e]
+        expect_ms = sum(30e-3 + (D - 1) * n * esz / (emu_gbps * 1e9) * 1e3 for n in units)
+        for i in range(P):
+            for step in range(steps):
+                assert res[i]["comm_ms"][step] >= 0.95 * expect_ms, (i, step, res[i]["comm_ms"][step], expect_ms)

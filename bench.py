@@ -320,7 +320,10 @@ def run_ours(args, c):
     # in-library comparison schedules, same workload (north_star: WeiPipe-style ring and FSDP-style global)
     if world > 1 and not args.no_baselines:
         out["baselines"] = {}
-        for name, Gb, sched in (("fsdp_global_D1", world, T.GWPS), ("weipipe_ring", 1, T.RING)):
+        runs = [("fsdp_global_D1", world, T.GWPS), ("weipipe_ring", 1, T.RING)]
+        if c["L"] % world == 0:   # NEXT-2: the paper-literal whole-layer owners with broadcast / reduce, same groups
+            runs.append(("paper_literal_bcast_reduce", G, T.LITERAL))
+        for name, Gb, sched in runs:
             T.bootstrap(rank, world, local, pg_backend="gloo")
             db = T.ModelDims(**{**dims.__dict__, "schedule": sched})
             sb = T.Session(world, Gb, db, N)

@@ -49,6 +49,14 @@ extern "C" {
                                    group_size 1); weights hop owner -> owner+1 -> ... around the ring,
                                    gradients accumulate hop by hop from owner+1 and end at the owner.
                                    The FSDP-style global schedule is group_size = n_devices (D = 1).     */
+#define TAWPIPE_LITERAL 4       /* paper-literal collectives (NEXT-2): whole
+                                   layers, device i of group k owns W_{(D·i+k) mod P} (layer l is shard
+                                   l mod P; needs L mod P = 0), E on device 0, F on device P−1.  Gather:
+                                   owner -> rail counterpart (k, i) of every other group (P2P), then
+                                   ncclBroadcast from (k, i) inside each group; reduction: ncclReduce to
+                                   (k, i) in each group, then P2P to the owner, which sums the D group
+                                   contributions and applies AdamW.  tawpipe_shard returns whole owned
+                                   units.  Exclusive with TAWPIPE_RING; combinable with TAWPIPE_NO_CCO.  */
 
 #define TAWPIPE_LEDGER_N 24     /* see tawpipe_ledger */
 #define TAWPIPE_STATS_N  16     /* see tawpipe_stats  */
@@ -69,7 +77,7 @@ typedef struct tawpipe_dims {
                           * then q|k|v, then h1, then the MLP's gu and y, per (layer, micro-batch);
                           * the recompute skips what was kept; results are bit-identical);
                           * 2 keep h_l only (full recompute)                                      */
-  int32_t schedule;      /* TAWPIPE_GWPS or TAWPIPE_RING, optionally | TAWPIPE_NO_CCO              */
+  int32_t schedule;      /* TAWPIPE_GWPS, TAWPIPE_RING or TAWPIPE_LITERAL, optionally | TAWPIPE_NO_CCO */
   int32_t reserved;      /* must be 0                                                            */
   float lr, beta1, beta2, adam_eps, weight_decay;   /* AdamW, torch semantics (R1)               */
   float rms_eps, rope_theta;                        /* 1e-5, 10000 (R10)                          */

@@ -117,3 +117,70 @@ def ring_ledger(L: int, P: int, d: int, s: int, e: int, f: int, r: int = 1) -> l
         reduce(units[l])
     reduce(E)
     return out
+
+
+def literal_ledger(L: int, P: int, D: int, d: int, x_block: int, x_e: int, x_f: int, r: int = 1) -> list:
+    """Paper-literal collective mode, by enumerating its transfers for device d.
+
+    Ownership (oracle/routes.py): layer l is shard l mod P, held whole by owner_table[l mod P]; the
+    holder / staging / exit device of a unit in group k is its rail counterpart (k, i) (R7); E lives on device 0
+    (i = 0), F on device P − 1 (i = G − 1).  A gather is the owner's P2P to (k, i) of every other group, then a
+    broadcast from (k, i) to its group ("broadcasts weight shard W_0 within group g_0 ... sends W_0 to
+    P_{P/D}"); a reduction is a reduce to (k, i) in every group, then (k, i)'s P2P to the owner (PAPER.md:127
+    "reduced to device P_{P/D−1}, and then transferred to P_{P−1}").  Every delivered copy of x is one transfer:
+    the receiver counts x received, the sender x sent (so a broadcast root sends (G−1)·x, reading R23).  Same step
+    sequence as the striped schedule; x_* are the whole (padded) unit lengths."""
+    from .routes import owner_table, rail_counterpart
+    G = P // D
+    own = owner_table(P, D)
+    out = [0] * N_COUNTERS
+
+    def xfer(kind, src, dst, cls_unit, n):
+        cls = "intra" if src // G == dst // G else "inter"
+        if dst == d:
+            out[index(kind, cls, "recv", cls_unit)] += n
+        if src == d:
+            out[index(kind, cls, "sent", cls_unit)] += n
+
+    def where(u):
+        cls_unit, l = u
+        if cls_unit == "block":
+            o = own[l % P]
+            hold = [rail_counterpart(l, kk, P, D) for kk in range(D)]
+            return o, hold, x_block
+        if cls_unit == "E":
+            return 0, [kk * G for kk in range(D)], x_e
+        return P - 1, [kk * G + G - 1 for kk in range(D)], x_f
+
+    def gather(u):
+        o, hold, n = where(u)
+        for h in hold:
+            if h != o:
+                xfer("w", o, h, u[0], n)
+        for h in hold:
+            for m in range((h // G) * G, (h // G) * G + G):
+                if m != h:
+                    xfer("w", h, m, u[0], n)
+
+    def reduce(u):
+        o, hold, n = where(u)
+        for h in hold:
+            for m in range((h // G) * G, (h // G) * G + G):
+                if m != h:
+                    xfer("g", m, h, u[0], n)
+        for h in hold:
+            if h != o:
+                xfer("g", h, o, u[0], n)
+
+    E, F = ("E", None), ("F", None)
+    gather(E)
+    for l in range(L):
+        gather(("block", l))
+    gather(F)
+    reduce(F)
+    for l in range(L - 1, -1, -1):
+        if not (r == 1 and l == L - 1):
+            gather(("block", l))
+        reduce(("block", l))
+    reduce(E)
+    return out

@@ -2,5 +2,5 @@
 
 The product is ``libtawpipe.so`` (C ABI in include/tawpipe.h); ``tawpipe.py`` is its ctypes binding.
 """
-from .tawpipe import (BF16, FP32, GWPS, NO_CCO, RING, ModelDims, Session, TawpipeError, bootstrap, lib,  # noqa: F401
+from .tawpipe import (BF16, FP32, GWPS, LITERAL, NO_CCO, RING, ModelDims, Session, TawpipeError, bootstrap, lib,  # noqa: F401
                       pack_full_model)

@@ -48,6 +48,9 @@ struct Unit {
   bool owned = false;
   int64_t off = 0;                  // offset of this rank's stripe in the owned-state arrays
   int64_t canon = 0;                // offset of the unit in the canonical full-model vector
+  int64_t lo = 0;                   // unit coordinate of this rank's owned piece (striped: j·s; whole units: 0)
+  int hold = 0;                     // TAWPIPE_LITERAL: member index of the owner inside its group and of the
+                                    // holder / staging / exit device inside every group (rail counterpart, R7)
   int n_nd = 0;
   int64_t nd_lo[2] = {0, 0}, nd_hi[2] = {0, 0};  // no-decay ranges (unit coordinates)
 };
@@ -89,7 +92,8 @@ struct Ctx {
   int H = 0, nh = 0, dh = 0, I = 0, V = 0, S = 0, Bm = 1;
   int64_t T = 0, phi = 0;
   bool bf = false;
-  bool ring = false;  // TAWPIPE_RING schedule
+  bool ring = false;     // TAWPIPE_RING schedule
+  bool literal = false;  // TAWPIPE_LITERAL: whole-layer owners, broadcast / reduce in the group (NEXT-2)
   size_t esz = 4;
   ncclComm_t wg = nullptr, wr = nullptr, gg = nullptr, gr = nullptr;
   cudaStream_t cs = nullptr, ws = nullptr, gs = nullptr;
@@ -328,6 +332,33 @@ void ledger_reduce_ring(const Unit& u, int d, int P, uint64_t* led) {
   if (d != (u.owner + 1) % P) led[ledger_index(K_G, C_INTER, D_RECV, u.cls)] += static_cast<uint64_t>(u.s);
   if (d != u.owner) led[ledger_index(K_G, C_INTER, D_SENT, u.cls)] += static_cast<uint64_t>(u.s);
 }
+// TAWPIPE_LITERAL (NEXT-2): whole units, owner (k_o, i), holder (k, i) in every group k.  Gather: rail P2P owner ->
+// (k, i) for k != k_o, then broadcast from (k, i) in each group.  Reduction: reduce to (k, i) in each group, then
+// rail P2P (k, i) -> owner for k != k_o.  Broadcast of x: each non-root receives x, the root sends (G−1)·x
+// (reading R23 of SURVEY App. A's "—"); reduce of x: the root receives (G−1)·x, each non-root sends x.
+void ledger_gather_literal(const Unit& u, int G, int D, int k, int j, uint64_t* led) {
+  const uint64_t x = static_cast<uint64_t>(u.n_pad);
+  if (D > 1 && j == u.hold) {
+    if (k == u.owner) led[ledger_index(K_W, C_INTER, D_SENT, u.cls)] += x * (D - 1);
+    else led[ledger_index(K_W, C_INTER, D_RECV, u.cls)] += x;
+  }
+  if (G > 1) {
+    if (j == u.hold) led[ledger_index(K_W, C_INTRA, D_SENT, u.cls)] += x * (G - 1);
+    else led[ledger_index(K_W, C_INTRA, D_RECV, u.cls)] += x;
+  }
+}
+void ledger_reduce_literal(const Unit& u, int G, int D, int k, int j, uint64_t* led) {
+  const uint64_t x = static_cast<uint64_t>(u.n_pad);
+  if (G > 1) {
+    if (j == u.hold) led[ledger_index(K_G, C_INTRA, D_RECV, u.cls)] += x * (G - 1);
+    else led[ledger_index(K_G, C_INTRA, D_SENT, u.cls)] += x;
+  }
+  if (D > 1 && j == u.hold) {
+    if (k == u.owner) led[ledger_index(K_G, C_INTER, D_RECV, u.cls)] += x * (D - 1);
+    else led[ledger_index(K_G, C_INTER, D_SENT, u.cls)] += x;
+  }
+}
+
 void ledger_reduce(const Unit& u, int G, int D, uint64_t* led) {
   if (G > 1) {
     led[ledger_index(K_G, C_INTRA, D_RECV, u.cls)] += static_cast<uint64_t>(u.s) * (G - 1);
@@ -368,6 +399,26 @@ void gather(int uid, void* dst) {
       if (emu_crosses(d, (d + 1) % P)) emu_delay(static_cast<double>(u.n_pad) * g->esz, g->ws);
     }
     ledger_gather_ring(u, d, P, g->ledger);
+    return;
+  }
+  if (g->literal) {  // NEXT-2: owner -> rail counterparts, then broadcast from the holder in every group
+    const bool holder = (g->j == u.hold);
+    if (g->D > 1 && holder) {
+      TP_NCCL(ncclGroupStart());
+      if (u.owned) {
+        for (int kk = 0; kk < g->D; ++kk)
+          if (kk != g->k) TP_NCCL(ncclSend(own, u.n_pad, wire_type(), kk, g->wr, g->ws));
+      } else {
+        TP_NCCL(ncclRecv(dst, u.n_pad, wire_type(), u.owner, g->wr, g->ws));
+      }
+      TP_NCCL(ncclGroupEnd());
+      if (emu_rail_crosses()) emu_delay(static_cast<double>(g->D - 1) * u.n_pad * g->esz, g->ws);
+    }
+    if (g->G > 1) {
+      TP_NCCL(ncclBroadcast(u.owned ? own : dst, dst, u.n_pad, wire_type(), u.hold, g->wg, g->ws));
+      if (emu_group_crosses()) emu_delay(static_cast<double>(g->G - 1) * u.n_pad * g->esz, g->ws);
+    }
+    ledger_gather_literal(u, g->G, g->D, g->k, g->j, g->ledger);
     return;
   }
   if (g->D > 1) {
@@ -437,6 +488,43 @@ void reduce_and_update(int uid, float* gacc) {
     return;
   }
   cudaStream_t s = g->gs;
+  if (g->literal) {  // NEXT-2: reduce to the holder in every group, holder -> owner on the rail, owner updates
+    const bool holder = (g->j == u.hold);
+    const void* partial = gacc;
+    bool part_f32 = true;
+    if (g->G > 1 || (g->D > 1 && !u.owned)) {
+      Timed t(s, 4, 0);
+      BY_TYPE(cast_f32<float>(gacc, (float*)g->gwire, u.n_pad, s), cast_f32<bf16>(gacc, (bf16*)g->gwire, u.n_pad, s));
+      partial = g->gwire;
+      part_f32 = false;
+    }
+    if (g->G > 1) {
+      Timed t(s, 6, 0);
+      TP_NCCL(ncclReduce(g->gwire, g->rsout, u.n_pad, wire_type(), ncclSum, u.hold, g->gg, s));
+      if (emu_group_crosses()) emu_delay(static_cast<double>(g->G - 1) * u.n_pad * g->esz, s);
+      partial = g->rsout;
+    }
+    if (g->D > 1 && holder) {
+      Timed t(s, 6, 0);
+      TP_NCCL(ncclGroupStart());
+      if (u.owned) {
+        int idx = 0;
+        for (int kk = 0; kk < g->D; ++kk)
+          if (kk != g->k) TP_NCCL(ncclRecv(wptr(g->crecv, (idx++) * u.n_pad), u.n_pad, wire_type(), kk, g->gr, s));
+      } else {
+        TP_NCCL(ncclSend(partial, u.n_pad, wire_type(), u.owner, g->gr, s));
+      }
+      TP_NCCL(ncclGroupEnd());
+      if (emu_rail_crosses()) emu_delay(static_cast<double>(g->D - 1) * u.n_pad * g->esz, s);
+    }
+    ledger_reduce_literal(u, g->G, g->D, g->k, g->j, g->ledger);
+    if (!u.owned) return;
+    const void* contrib[8];
+    int idx = 0;
+    for (int kk = 0; kk < g->D; ++kk) contrib[kk] = (kk == g->k) ? partial : wptr(g->crecv, (idx++) * u.n_pad);
+    adam_update(u, contrib, g->D, g->k, part_f32);
+    return;
+  }
   const void* own_partial = gacc;
   bool own_f32 = true;
   if (g->G > 1 || (g->D > 1 && !u.owned)) {
@@ -484,7 +572,7 @@ void adam_update(const Unit& u, const void* const* contrib, int n_contrib, int o
   hp.wd = g->dims.weight_decay;
   hp.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta1), g->step_t));
   hp.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta2), g->step_t));
-  const int64_t stripe_off = static_cast<int64_t>(g->j) * u.s;
+  const int64_t stripe_off = u.lo;
   Timed t(s, 2, (2.0 * n_contrib * g->esz + 26.0) * u.s);
   BY_TYPE(adamw_fused<float>(contrib, n_contrib, own_k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
                              (float*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s),
@@ -904,7 +992,12 @@ void validate(int P, int G, int L, const tawpipe_dims* d, int N, int world) {
   TP_CHECK(d->dtype == TAWPIPE_FP32 || d->dtype == TAWPIPE_BF16, TAWPIPE_ECONFIG, "dtype must be FP32 or BF16");
   TP_CHECK(d->reserved == 0, TAWPIPE_ECONFIG, "reserved must be 0");
   TP_CHECK(d->ckpt >= 0 && d->ckpt <= 2, TAWPIPE_ECONFIG, "ckpt must be 0, 1 or 2");
-  TP_CHECK((d->schedule & ~(TAWPIPE_NO_CCO | TAWPIPE_RING)) == 0, TAWPIPE_ECONFIG, "unknown schedule flag");
+  TP_CHECK((d->schedule & ~(TAWPIPE_NO_CCO | TAWPIPE_RING | TAWPIPE_LITERAL)) == 0, TAWPIPE_ECONFIG,
+           "unknown schedule flag");
+  TP_CHECK(!((d->schedule & TAWPIPE_RING) && (d->schedule & TAWPIPE_LITERAL)), TAWPIPE_ECONFIG,
+           "TAWPIPE_RING and TAWPIPE_LITERAL are exclusive");
+  TP_CHECK(!(d->schedule & TAWPIPE_LITERAL) || L % P == 0, TAWPIPE_ECONFIG,
+           "TAWPIPE_LITERAL needs L mod P == 0 (one whole shard per device, PAPER.md:123)");
   TP_CHECK(!(d->schedule & TAWPIPE_RING) || G == 1, TAWPIPE_ECONFIG,
            "TAWPIPE_RING owns whole layers per device: group_size must be 1");
   if (d->dtype == TAWPIPE_BF16) {
@@ -921,9 +1014,9 @@ struct Plan {
   std::vector<Unit> units;
   int64_t owned_total = 0, max_pad = 0, max_s = 0;
 };
-Plan make_plan(int P, int G, int L, int64_t H, int64_t I, int64_t V, int rank) {
+Plan make_plan(int P, int G, int L, int64_t H, int64_t I, int64_t V, int rank, bool literal) {
   Plan pl;
-  const int D = P / G, k = rank / G;
+  const int D = P / G, k = rank / G, j = rank % G;
   const int64_t phi = 4 * H * H + 3 * H * I + 2 * H;
   pl.units.assign(L + 2, Unit{});
   for (int l = 0; l < L + 2; ++l) {
@@ -952,9 +1045,20 @@ Plan make_plan(int P, int G, int L, int64_t H, int64_t I, int64_t V, int rank) {
       u.nd_lo[0] = 0;
       u.nd_hi[0] = H;
     }
-    u.n_pad = pad_to(u.n, G);
-    u.s = u.n_pad / G;
-    u.owned = (u.owner == k);
+    if (literal) {
+      // device i of group k holds W_{(D·i+k) mod P}; layer l (L mod P = 0) is shard l mod P, i.e.
+      // group l mod D, member (l / D) mod G -- the rail counterpart of every group (R7).  E: device 0, F: P − 1.
+      u.hold = l < L ? (l / D) % G : (l == L ? 0 : G - 1);
+      u.n_pad = pad_to(u.n, 1);
+      u.s = u.n_pad;
+      u.owned = (u.owner == k && u.hold == j);
+      u.lo = 0;
+    } else {
+      u.n_pad = pad_to(u.n, G);
+      u.s = u.n_pad / G;
+      u.owned = (u.owner == k);
+      u.lo = static_cast<int64_t>(j) * u.s;
+    }
     pl.max_pad = std::max(pl.max_pad, u.n_pad);
     pl.max_s = std::max(pl.max_s, u.s);
   }
@@ -989,11 +1093,12 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   c.T = static_cast<int64_t>(c.Bm) * c.S;
   c.bf = d->dtype == TAWPIPE_BF16;
   c.ring = (d->schedule & TAWPIPE_RING) != 0;
+  c.literal = (d->schedule & TAWPIPE_LITERAL) != 0;
   c.esz = c.bf ? 2 : 4;
   const int64_t H = c.H, I = c.I, V = c.V;
   c.phi = 4 * H * H + 3 * H * I + 2 * H;
   {
-    Plan pl = make_plan(P, G, L, H, I, V, c.rank);
+    Plan pl = make_plan(P, G, L, H, I, V, c.rank, (d->schedule & TAWPIPE_LITERAL) != 0);
     c.units = pl.units;
     c.owned_total = pl.owned_total;
     c.max_pad = pl.max_pad;
@@ -1132,7 +1237,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   for (int l = 0; l < L + 2; ++l) {
     const Unit& u = c.units[l];
     if (!u.owned) continue;
-    const int64_t lo = static_cast<int64_t>(c.j) * u.s;  // stripe start in unit coordinates
+    const int64_t lo = u.lo;  // owned piece's start in unit coordinates
     float* ms = c.master + u.off;
     BY_TYPE(init_normal<float>((float*)wptr(c.wire, u.off), ms, u.s, u.canon + lo, d->seed, 0.02f, c.cs),
             init_normal<bf16>((bf16*)wptr(c.wire, u.off), ms, u.s, u.canon + lo, d->seed, 0.02f, c.cs));
@@ -1159,7 +1264,7 @@ void load(const float* full, int64_t n) {
   for (int l = 0; l < c.L + 2; ++l) {
     const Unit& u = c.units[l];
     if (!u.owned) continue;
-    const int64_t lo = static_cast<int64_t>(c.j) * u.s;
+    const int64_t lo = u.lo;
     float* ms = c.master + u.off;
     // every copy is ordered on c.cs: the compute stream is non-blocking and would not see legacy-stream copies
     TP_CUDA(cudaMemsetAsync(ms, 0, u.s * 4, c.cs));
@@ -1246,16 +1351,19 @@ int tawpipe_plan(int n_devices, int group_size, int n_layers, const tawpipe_dims
     validate(n_devices, group_size, n_layers, dims, n_micro, n_devices);
     TP_CHECK(rank >= 0 && rank < n_devices, TAWPIPE_ECONFIG, "rank out of range");
     const int G = group_size, D = n_devices / group_size, L = n_layers;
-    Plan pl = make_plan(n_devices, G, L, dims->hidden, dims->ffn, dims->vocab, rank);
+    const bool literal = (dims->schedule & TAWPIPE_LITERAL) != 0;
+    Plan pl = make_plan(n_devices, G, L, dims->hidden, dims->ffn, dims->vocab, rank, literal);
     uint64_t led[TAWPIPE_LEDGER_N] = {};
     const bool ring = (dims->schedule & TAWPIPE_RING) != 0;
     const int P = n_devices;
     auto gat = [&](const Unit& u) {
       if (ring) ledger_gather_ring(u, rank, P, led);
+      else if (literal) ledger_gather_literal(u, G, D, rank / G, rank % G, led);
       else ledger_gather(u, G, D, led);
     };
     auto red = [&](const Unit& u) {
       if (ring) ledger_reduce_ring(u, rank, P, led);
+      else if (literal) ledger_reduce_literal(u, G, D, rank / G, rank % G, led);
       else ledger_reduce(u, G, D, led);
     };
     // the step's communication sequence (run_step): E gather, forward gathers 0..L-1, F gather, F reduction,

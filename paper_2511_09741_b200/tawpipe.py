@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libtawpipe.so")
 
 OK, ECONFIG, EINVARIANT, ERUNTIME, EUNINIT = 0, -2, -3, -4, -5
 FP32, BF16 = 0, 1
-GWPS, NO_CCO, RING = 0, 1, 2
+GWPS, NO_CCO, RING, LITERAL = 0, 1, 2, 4
 LEDGER_N, STATS_N = 24, 16
 
 STATS_NAMES = ("step_ms", "exposed_comm_ms", "weight_comm_ms", "grad_comm_ms", "gemm_ms", "gemm_gflop",

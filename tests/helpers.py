@@ -39,7 +39,17 @@ def owner_group(uid, L, D):
     return uid % D
 
 
-def reassemble(cfg: om.ModelConfig, P: int, G: int, shards: list) -> dict:
+def literal_owner(uid, P: int, D: int) -> int:
+    """TAWPIPE_LITERAL owner device (PAPER.md:123 shard map via oracle/routes.py; E on 0, F on P − 1)."""
+    from oracle import routes
+    if uid == "E":
+        return 0
+    if uid == "F":
+        return P - 1
+    return routes.owner_table(P, D)[uid % P]
+
+
+def reassemble(cfg: om.ModelConfig, P: int, G: int, shards: list, literal: bool = False) -> dict:
     """Rebuild full fp64 params from every rank's tawpipe_shard output (include/tawpipe.h order)."""
     D = P // G
     vecs = {}
@@ -48,15 +58,22 @@ def reassemble(cfg: om.ModelConfig, P: int, G: int, shards: list) -> dict:
     for rank in range(P):
         k = rank // G
         for uid, n in unit_list(cfg):
-            if owner_group(uid, cfg.n_layers, D) != k:
-                continue
-            s = OL.padded(n, G) // G
-            pieces[(uid, rank % G)] = shards[rank][cursors[rank]:cursors[rank] + s]
+            if literal:   # whole units on their owner device
+                if literal_owner(uid, P, D) != rank:
+                    continue
+                s = OL.padded(n, 1)
+                pieces[(uid, 0)] = shards[rank][cursors[rank]:cursors[rank] + s]
+            else:
+                if owner_group(uid, cfg.n_layers, D) != k:
+                    continue
+                s = OL.padded(n, G) // G
+                pieces[(uid, rank % G)] = shards[rank][cursors[rank]:cursors[rank] + s]
             cursors[rank] += s
     for rank in range(P):
         assert cursors[rank] == len(shards[rank]), (rank, cursors[rank], len(shards[rank]))
     for uid, n in unit_list(cfg):
-        vecs[uid] = np.concatenate([pieces[(uid, j)] for j in range(G)])[:n].astype(np.float64)
+        parts = [pieces[(uid, 0)]] if literal else [pieces[(uid, j)] for j in range(G)]
+        vecs[uid] = np.concatenate(parts)[:n].astype(np.float64)
     fn, head = OL.unflatten_F(vecs["F"], cfg)
     return {"embed": vecs["E"].reshape(cfg.vocab, cfg.hidden),
             "layers": [OL.unflatten_layer(vecs[l], cfg) for l in range(cfg.n_layers)],

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--ckpt", type=int, default=0)
     ap.add_argument("--no-cco", action="store_true")
     ap.add_argument("--ring", action="store_true")
+    ap.add_argument("--literal", action="store_true")
     ap.add_argument("--emu-gbps", type=float, default=0.0)   # NEXT-3 emulated inter-node link
     ap.add_argument("--emu-node", type=int, default=0)
     ap.add_argument("--out", required=True)
@@ -35,7 +36,8 @@ def main():
     params = synth.perturb_gains(synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab))
     dims = T.ModelDims(n_layers=cfg.n_layers, hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, vocab=cfg.vocab,
                        seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=a.dtype, ckpt=a.ckpt,
-                       schedule=(T.NO_CCO if a.no_cco else T.GWPS) | (T.RING if a.ring else 0))
+                       schedule=(T.NO_CCO if a.no_cco else T.GWPS) | (T.RING if a.ring else 0)
+                       | (T.LITERAL if a.literal else 0))
     sess = T.Session(world, a.G, dims, a.N)
     sess.load(T.pack_full_model(params))
     if a.emu_gbps > 0:

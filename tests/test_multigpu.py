@@ -35,6 +35,11 @@ CASES = [
     # NEXT-3: 2 emulated nodes of 2 at 0.05 GB/s: same results and ledger, paced rail traffic
     ("c0-2x2-emu", C0, 4, 2, 2, 4, 0, 0, False, False, 0.05, 2),
     ("c0-ring4-emu", C0, 4, 1, 4, 4, 0, 0, False, True, 0.05, 2),
+    # NEXT-2 paper-literal collectives (ring field = "literal"): whole-layer owners, broadcast / reduce in groups
+    ("c0-literal-2x2", C0, 4, 2, 4, 4, 0, 0, False, "literal"),
+    ("c0-literal-4x1", C0, 4, 1, 4, 4, 0, 1, False, "literal"),
+    ("c0b-literal-1x4-bf16", C0B, 4, 4, 4, 4, 1, 0, False, "literal"),
+    ("c0-literal-2x2-emu", C0, 4, 2, 4, 4, 0, 0, False, "literal", 0.05, 2),
 ]
 CASES = [c if len(c) == 12 else c + (0.0, 0) for c in CASES]
 
@@ -48,6 +53,8 @@ def free_port():
 @pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco,ring,emu_gbps,emu_node", CASES,
                          ids=[c[0] for c in CASES])
 def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco, ring, emu_gbps, emu_node):
+    literal = ring == "literal"
+    ring = ring is True
     if not torch.cuda.is_available() or torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     cfg = oracle_cfg(base, n_layers=L)
@@ -56,7 +63,7 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--cfg", json.dumps(dict(base, n_layers=L)), "--G", str(G), "--N", str(N), "--steps", str(steps),
            "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else []) \
-        + (["--ring"] if ring else []) + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
+        + (["--ring"] if ring else []) + (["--literal"] if literal else []) + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
@@ -74,17 +81,22 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
             assert abs(res[i]["losses"][step] - lr) / lr <= tol_loss, (i, step, res[i]["losses"][step], lr)
         if step == 0:
             theta1 = {k: v for k, v in st.params.items()}
-    gpu = reassemble(cfg, P, G, [x["shard"] for x in res])
+    gpu = reassemble(cfg, P, G, [x["shard"] for x in res], literal=literal)
     et, ed, viol, off, rep = weight_errors(gpu, st.params, theta0, grads, cfg, kappa)
     assert et <= tol_w and viol == 0, (et, viol, sorted(rep, key=lambda z: -z[1])[:3])
     # byte ledger: bit-exact against the closed forms, every rank, every step
     H, V = cfg.hidden, cfg.vocab
     s, e, f = (OL.padded(n, G) // G for n in (om.phi(cfg), V * H, H + V * H))
     for i in range(P):
-        expect = LG.ring_ledger(L, P, i, s, e, f, r=1) if ring else LG.closed_form(L, P, G, i // G, s, e, f, r=1)
+        if ring:
+            expect = LG.ring_ledger(L, P, i, s, e, f, r=1)
+        elif literal:
+            expect = LG.literal_ledger(L, P, P // G, i, *(OL.padded(n, 1) for n in (om.phi(cfg), V * H, H + V * H)))
+        else:
+            expect = LG.closed_form(L, P, G, i // G, s, e, f, r=1)
         for step in range(steps):
             assert [int(x) for x in res[i]["ledgers"][step]] == expect, (i, step)
-    if emu_gbps and not ring:
+    if emu_gbps and not ring and not literal:
         # NEXT-3 pacing: every rail exchange (D > 1, groups = emulated nodes) adds 30 µs + (D−1)·stripe bytes / bw
         # to each participant's comm stream: gathers E, L blocks, F and L−1 re-gathers; reductions F, L blocks, E
         D, esz = P // G, (4 if dtype == 0 else 2)

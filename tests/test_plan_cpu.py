@@ -124,3 +124,58 @@ def test_ring_requires_group_size_1(T):
     with pytest.raises(T.TawpipeError) as ei:
         T.plan(4, 2, d, 4, 0)
     assert "group_size" in str(ei.value)
+
+
+LITERAL_GRID = [(1, 1, 2), (2, 1, 2), (2, 2, 2), (4, 2, 4), (4, 4, 4), (4, 1, 4), (6, 3, 6), (6, 2, 6), (6, 3, 12),
+                (8, 2, 8), (8, 4, 16), (8, 8, 8), (8, 1, 8)]
+
+
+@pytest.mark.parametrize("P,G,L", LITERAL_GRID)
+def test_literal_plan_ledger_and_identities(T, P, G, L):
+    """NEXT-2 paper-literal mode: the plan's ledger equals the enumerated definition (oracle/ledger.py over
+    oracle/routes.py's PAPER.md:123 map), every device receives 3L(P−1)φ/P block elements at r = 0 (SURVEY App. A:
+    the same as the striped mode), and each device owns exactly L/P whole layers."""
+    cfg = oracle_cfg(C0, n_layers=L)
+    H, V = cfg.hidden, cfg.vocab
+    x, e, f = OL.padded(om.phi(cfg), 1), OL.padded(V * H, 1), OL.padded(H + V * H, 1)
+    D = P // G
+    d = dims_for(T, cfg)
+    d.schedule = T.LITERAL
+    for rank in range(P):
+        led, n = T.plan(P, G, d, P, rank)
+        assert led == LG.literal_ledger(L, P, D, rank, x, e, f, r=1), (rank, [(LG.name(i), a, b) for i, (a, b) in
+                                                                       enumerate(zip(led, LG.literal_ledger(
+                                                                           L, P, D, rank, x, e, f, r=1))) if a != b])
+        r0 = LG.literal_ledger(L, P, D, rank, x, e, f, r=0)
+        assert LG.block_received(r0) * P == 3 * L * (P - 1) * x
+        assert n == (L // P) * x + (e if rank == 0 else 0) + (f if rank == P - 1 else 0)
+
+
+def test_literal_paper_example_p6_d2(T):
+    """PAPER.md:127 worked example, P = 6, D = 2 (tests/golden/paper_fig3_routes.txt): W_5 is owned by P_5; its
+    gradient computed in g_0 is reduced to P_2 and transferred to P_5 -- so in the backward of layer 5, P_2 sends one
+    whole layer on the rail and P_5 receives one; in the forward P_0 broadcasts W_0 in g_0 and sends it to P_3."""
+    cfg = oracle_cfg(C0, n_layers=6)
+    x = OL.padded(om.phi(cfg), 1)
+    d = dims_for(T, cfg)
+    d.schedule = T.LITERAL
+    led = {r: T.plan(6, 3, d, 6, r)[0] for r in range(6)}
+    # one layer per device; every layer is gathered twice but layer 5 (r = 1) -> owner P_5 sends layer 5 once on
+    # the rail (forward) and P_0 sends layer 0 twice (forward + backward)
+    assert led[0][LG.index("w", "inter", "sent", "block")] == 2 * x
+    assert led[5][LG.index("w", "inter", "sent", "block")] == 1 * x
+    assert led[5][LG.index("g", "inter", "recv", "block")] == 1 * x     # W_5's gradient from g_0 (via P_2)
+    assert led[2][LG.index("g", "inter", "sent", "block")] == 1 * x     # P_2 = P_{P/D-1} exits W_5's gradient of g_0
+    assert led[2][LG.index("g", "inter", "recv", "block")] == 1 * x     # P_2 owns W_4: receives g_1's partial (P_5)
+
+
+def test_literal_requires_l_mod_p(T):
+    cfg = oracle_cfg(C0, n_layers=2)
+    d = dims_for(T, cfg)
+    d.schedule = T.LITERAL
+    with pytest.raises(T.TawpipeError) as ei:
+        T.plan(4, 2, d, 4, 0)
+    assert "L mod P" in str(ei.value)
+    d.schedule = T.LITERAL | T.RING
+    with pytest.raises(T.TawpipeError):
+        T.plan(2, 1, d, 2, 0)

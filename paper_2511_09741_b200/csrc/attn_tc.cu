@@ -73,6 +73,9 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -794,6 +797,262 @@ __global__ void __launch_bounds__(224, 1)
   }
 }
 
+// ----------------------------------------------------------------------------------------------- forward v5
+// Two query tiles per CTA (A = 2p+1, B = 2p: the same K/V stream, A one key tile longer) with one softmax
+// warpgroup each, so that one tile's exponentials run on the MUFU while the other tile's scores are loaded,
+// reduced and written back (ping-pong across tiles instead of within one).  Each tile has one S/P buffer and one
+// O accumulator in TMEM (4 × 128 columns); S_t(j) is issued right behind P·V_t(j−1) by the same thread, so its
+// completion implies P·V_t(j−1)'s: O_t is stable whenever softmax t runs and the lazy rescale never waits.
+//   warps 0-3: softmax of tile A, warps 4-7: softmax of tile B (thread = row, lane quarter = warp % 4)
+//   warp 8: MMA issuer (P·V_t(j) then S_t(j+1), in order), warp 9: TMA producer (Q_A, Q_B once; K, V 2-stage rings)
+//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
+template <int DH>
+struct Fwd5Smem {
+  static constexpr int QB = DH / 64 * ATOM;
+  static constexpr int NST = 2;
+  static constexpr int OFF_Q = 0;   // Q_A, Q_B
+  static constexpr int OFF_K = 2 * QB;
+  static constexpr int OFF_V = 2 * QB + NST * QB;
+  static constexpr int OFF_BAR = 2 * QB + 2 * NST * QB;
+  static constexpr int BYTES = OFF_BAR + 256;
+};
+
+// 320 threads; the bounds say 384 so that ptxas keeps to 168 registers (three warps share SMSPs 0 and 1)
+template <int DH>
+__global__ void __launch_bounds__(384, 1)
+    fa_fwd5_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
+                   int nh, float scale2, unsigned long long* __restrict__ trace) {
+  auto TR = [&](int it, int ev) {
+    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32) trace[it * 16 + ev] = clock64();
+  };
+  using L = Fwd5Smem<DH>;
+  constexpr int NST = L::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
+           *v_empty = bar + 1 + 3 * NST, *s_full = bar + 1 + 4 * NST, *p_ready = bar + 3 + 4 * NST,
+           *pv_done = bar + 5 + 4 * NST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7 + 4 * NST);
+
+  const int n_pairs = S / BQ / 2;
+  // head-major (K/V of a head stay in L2), heaviest pairs first within a head
+  const int pr = n_pairs - 1 - static_cast<int>(blockIdx.x % n_pairs);
+  const int h = static_cast<int>(blockIdx.x / n_pairs);
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int n_kv_A = 2 * pr + 2;   // tile B (2p) stops one key tile earlier
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(sm) & 1023) __trap();
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_ready[t], 128);
+      mbar_init(&pv_done[t], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 9) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * L::QB);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_Q + t * L::QB + a * ATOM, &tm, q_full, h * DH + a * 64,
+                      row0 + (2 * pr + 1 - t) * BQ);
+      for (int j = 0; j < n_kv_A; ++j) {
+        const int st = j % NST;
+        const uint32_t ph = (j / NST) & 1;
+        mbar_wait_sleep(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
+        mbar_wait_sleep(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
+                      row0 + j * BQ);
+      }
+    }
+  } else if (warp == 8) {
+    // one issuer for both chains, in the order P·V_t(j), S_t(j+1) per tile: the tensor pipe executes one thread's
+    // MMAs in order, so S_t(j+1) overwrites tile t's P only after P·V_t(j) has read it, with no wait in between
+    constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
+    constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
+    auto issue_s = [&](int t, int jj) {
+      const uint32_t sK = smem_u32(sm + L::OFF_K + (jj % NST) * L::QB);
+      const uint32_t sQ = smem_u32(sm + L::OFF_Q + t * L::QB);
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tmem + t * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
+      umma_commit_w(&s_full[t]);
+      TR(jj, 6 + t);
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(&k_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    umma_commit_w(&k_empty[0]);
+    for (int j = 0; j < n_kv_A; ++j) {
+      const int st = j % NST;
+      mbar_wait(&v_full[st], (j / NST) & 1);
+      const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
+      const bool next = j + 1 < n_kv_A;
+      if (next) mbar_wait(&k_full[(j + 1) % NST], ((j + 1) / NST) & 1);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (j >= n_kv_A - t) continue;   // tile B has one key tile fewer
+        mbar_wait(&p_ready[t], j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          umma_f16_tmemA_w(tmem + 256 + t * 128, tmem + t * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
+        umma_commit_w(&pv_done[t]);
+        TR(j, 8 + t);
+        if (j + 1 < n_kv_A - t) issue_s(t, j + 1);
+      }
+      umma_commit_w(&v_empty[st]);
+      if (next) umma_commit_w(&k_empty[(j + 1) % NST]);
+    }
+  } else {
+    const int t = warp >> 2;          // 0: tile A, 1: tile B
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int qt = 2 * pr + 1 - t;
+    const int n_kv = qt + 1;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
+    float m2 = -INFINITY, l = 0.f;
+    float s[128];
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      if (r == 0) TR(j, 3 * t);
+      tc_fence_after();
+      {
+        uint32_t u0[32], u1[32], u2[32], u3[32];
+        tmem_ld32(tS, u0);
+        tmem_ld32(tS + 32, u1);
+        tmem_ld32(tS + 64, u2);
+        tmem_ld32(tS + 96, u3);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(u0[i]);
+          s[32 + i] = __uint_as_float(u1[i]);
+          s[64 + i] = __uint_as_float(u2[i]);
+          s[96 + i] = __uint_as_float(u3[i]);
+        }
+      }
+      if (j == qt) {  // diagonal tile only
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > r) s[i] = -INFINITY;
+      }
+      float mxa[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mxa[k] = s[k];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+      mx *= scale2;
+      if (j == 0) {
+        m2 = mx;
+      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
+        // lazy rescale; O_t is stable here (S_t(j) was issued after P·V_t(j−1) completed)
+        const float mnew = fmaxf(m2, mx);
+        const float alpha = ex2(m2 - mnew);
+        l *= alpha;
+#pragma unroll 1
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld32(tO + c * 32, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st32(tO + c * 32, u);
+        }
+        m2 = mnew;
+      }
+      // ping-pong: the two tiles take turns on the exponential pass (A_j, B_j, A_{j+1}, ...), so that one tile's
+      // loads / max / rescale / P store overlap the other tile's MUFU work (named barriers 1: A may go, 2: B may go)
+      if (t == 0) {
+        if (j > 0) named_bar(1, 256);
+      } else {
+        named_bar(2, 256);
+      }
+      if (r == 0) TR(j, 3 * t + 1);
+      float2 sa2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(-m2, -m2);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pw[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float2 a2 = ffma2(make_float2(s[c * 32 + i], s[c * 32 + i + 1]), sc2, nm2);
+          const float p0 = ex2(a2.x), p1 = ex2(a2.y);
+          sa2[(i >> 1) & 3] = fadd2(sa2[(i >> 1) & 3], make_float2(p0, p1));
+          pw[i / 2] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + c * 16, pw);
+      }
+      if (r == 0) TR(j, 3 * t + 2);
+      if (t == 0) {
+        if (j < n_kv - 1) named_bar_arrive(2, 256);   // B's step j (tile B has n_kv − 1 steps)
+      } else {
+        named_bar_arrive(1, 256);                     // A's step j + 1
+      }
+      const float2 t2 = fadd2(fadd2(sa2[0], sa2[1]), fadd2(sa2[2], sa2[3]));
+      l += t2.x + t2.y;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_ready[t]);
+    }
+    mbar_wait(&pv_done[t], (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tO + c * 32, u);
+      tmem_wait_ld();
+      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 o;
+        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
+        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
+        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
+        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
+        d4[v] = o;
+      }
+    }
+    lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ----------------------------------------------------------------------------------------------- forward v4
 // As v3, but the row softmax is split over two warps per SMSP: warp w (w = 2..9) handles rows 32(w%4).. and
 // key columns 64·h.. (h = half).  The two halves exchange their partial row maxima through smem once per
@@ -1077,7 +1336,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *do_full = bar + 5, *do_empty = bar + 6,
            *s_full = bar + 7, *dp_full = bar + 8, *tdp_free = bar + 9, *p_ready = bar + 10, *ds_ready = bar + 11,
-           *mm2_done = bar + 12;
+           *mm2_done = bar + 12, *dq_done = bar + 13;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
   float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
   float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
@@ -1110,6 +1369,7 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(p_ready, 128);
     mbar_init(ds_ready, 128);
     mbar_init(mm2_done, 1);
+    mbar_init(dq_done, 1);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -1181,13 +1441,15 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(ds_ready, it & 1);
         TR(it, 3);
         // Pᵀ_it fully consumed (dV issued before, dS pass done): Sᵀ_{it+1} goes first so that the softmax warps
-        // compute Pᵀ_{it+1} while dK_it and dQ_it run on the tensor core
+        // compute Pᵀ_{it+1} while dQ_it and dK_it run on the tensor core.  dQ_it precedes dK_it: its drain (which
+        // frees the TMEM columns dPᵀ_{it+1} needs) then overlaps dK_it instead of following it
         if (it + 1 < n_it) issue_s(it + 1);
         tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
-#pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
+        umma_commit_w(dq_done);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
         umma_commit_w(&q_empty[st]);
         umma_commit_w(mm2_done);
       }
@@ -1319,7 +1581,7 @@ __global__ void __launch_bounds__(320, 1)
     uint8_t* stg = sm + L::OFF_STG;
     for (int it = 0; it < n_it; ++it) {
       const int i = jt + it;
-      mbar_wait(mm2_done, it & 1);   // dQ_i complete
+      mbar_wait(dq_done, it & 1);    // dQ_i complete
       if (t == 0) TR(it, 9);
       tc_fence_after();
       uint32_t u[DH / 32][32];
@@ -1414,10 +1676,44 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
   const int H = nh * dh;
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, static_cast<int64_t>(B) * S, 3ll * H, 128);
   const float scale2 = LOG2E / sqrtf(static_cast<float>(dh));
-  static const int fwd_ver = [] {
+  static const int fwd_env = [] {
     const char* e = std::getenv("TAWPIPE_FA_FWD");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 5;
   }();
+  static unsigned long long* ftrace = [] {
+    unsigned long long* p = nullptr;
+    if (std::getenv("TAWPIPE_FA_TRACE")) {
+      cudaMalloc(&p, 32 * 16 * 8);
+      cudaMemset(p, 0, 32 * 16 * 8);
+    }
+    return p;
+  }();
+  // v5 pairs query tiles: needs an even number of them (else v3)
+  const int fwd_ver = (fwd_env == 5 && (S / BQ) % 2 != 0) ? 3 : fwd_env;
+  if (fwd_ver == 5) {
+    dim3 grid5(static_cast<unsigned>((S / BQ / 2) * nh), static_cast<unsigned>(B));
+    if (dh == 128) {
+      static bool once = (prep(fa_fwd5_kernel<128>, Fwd5Smem<128>::BYTES), true);
+      (void)once;
+      fa_fwd5_kernel<128><<<grid5, 320, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);
+    } else {
+      static bool once = (prep(fa_fwd5_kernel<64>, Fwd5Smem<64>::BYTES), true);
+      (void)once;
+      fa_fwd5_kernel<64><<<grid5, 320, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);
+    }
+    TP_CUDA(cudaGetLastError());
+    g_kstats.launches++;
+    if (ftrace) {
+      unsigned long long hb[32 * 16];
+      TP_CUDA(cudaMemcpy(hb, ftrace, sizeof(hb), cudaMemcpyDeviceToHost));
+      const unsigned long long t0 = hb[0];
+      auto T = [&](int it, int e) { return (long long)(hb[it * 16 + e] - t0); };
+      for (int it = 0; it < 12; ++it)
+        std::fprintf(stderr, "fwd5 j %2d: A s_full=%lld exp=%lld..%lld | B s_full=%lld exp=%lld..%lld | S_A=%lld S_B=%lld PV_A=%lld PV_B=%lld\n",
+                     it, T(it, 0), T(it, 1), T(it, 2), T(it, 3), T(it, 4), T(it, 5), T(it, 6), T(it, 7), T(it, 8), T(it, 9));
+    }
+    return;
+  }
   if (fwd_ver == 4) {
     dim3 grid4(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
     if (dh == 128) {
@@ -1433,14 +1729,7 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
     g_kstats.launches++;
     return;
   }
-  static unsigned long long* ftrace = [] {
-    unsigned long long* p = nullptr;
-    if (std::getenv("TAWPIPE_FA_TRACE")) {
-      cudaMalloc(&p, 32 * 16 * 8);
-      cudaMemset(p, 0, 32 * 16 * 8);
-    }
-    return p;
-  }();
+
   if (fwd_ver == 3) {
     static const int emu = [] {
       const char* e = std::getenv("TAWPIPE_FA_EMU");   // exponentials per 8 computed on the FMA pipe

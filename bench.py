@@ -55,6 +55,16 @@ def flops_per_token(c, recompute=True):
     return f
 
 
+def traffic_for(kernel):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+            t = json.load(fh)[kernel]
+        return {"traffic": t["bytes"], "traffic_per": t["per"], "traffic_source": t["source"]}
+    except Exception:
+        return {"traffic": None}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -303,7 +313,7 @@ def run_ours(args, c):
             / (peaks["bf16_tflops"] * 1e12) * 1e3 / ms,
             "hfu_full_recompute": flops_per_token(c) * c["m"] * c["B"] * c["S"] / (peaks["bf16_tflops"] * 1e12) * 1e3 / ms},
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                     "frac": ach / peak, "traffic": None,
+                     "frac": ach / peak, **traffic_for(dom),
                      "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
                      "share_of_step": dom_ms / ms},
         "kernel_ms": {"gemm": st["gemm_ms"], "attention": st["attn_ms"], "adamw": st["adamw_ms"],

@@ -152,6 +152,25 @@ def attention_bwd(do, q, k, v, o, P):
     return dq, dk, dv
 
 
+def attention_row(i, q_i, k, v, do_i):
+    """One query row of attention_fwd / attention_bwd for one head, for spot checks at sizes where the S×S
+    matrices do not fit: keys 0..i only (causal), the same definitions row by row.  q_i, do_i [d_h];
+    k, v [S, d_h].  Returns (o_i, lse_i, dq_i) with lse_i = log Σ_j exp(c·q_i·k_j)."""
+    dh = q_i.shape[0]
+    c = 1.0 / np.sqrt(dh)
+    s = c * (k[: i + 1] @ q_i)
+    mx = s.max()
+    e = np.exp(s - mx)
+    lse = mx + np.log(e.sum())
+    p = e / e.sum()
+    o_i = p @ v[: i + 1]
+    dP = v[: i + 1] @ do_i
+    delta = float(do_i @ o_i)
+    dS = p * (dP - delta)
+    dq_i = c * (dS @ k[: i + 1])
+    return o_i, lse, dq_i
+
+
 def sigmoid(u):
     return 1.0 / (1.0 + np.exp(-u))
 

@@ -149,3 +149,66 @@ def test_attention_bf16_matches_oracle(T, B, S, nh, dh):
     ro, rl, rd = oracle_attention(tq, tdo, B, S, nh, dh)
     assert rel(o, ro) < 2e-2 and rel(lse, rl) < 1e-2 and rel(dqkv, rd) < 3e-2, (rel(o, ro), rel(lse, rl),
                                                                               rel(dqkv, rd))
+
+
+# ---------------------------------------------------------------------------------------------- full size
+# BASELINE.json's full size, in the launch configuration bench.py times (C3: one 32,768-token sequence, 32 heads,
+# d_h = 128; QKV and gate/up-wgrad GEMM shapes): outputs sampled where the oracle can compute them one by one.
+
+def test_attention_full_size_sampled_rows(T):
+    B, S, nh, dh = 1, 32768, 32, 128
+    H = nh * dh
+    g = torch.Generator(device="cuda").manual_seed(21)
+    tq = (torch.randn((S, 3 * H), generator=g, device="cuda") * 0.5).bfloat16()
+    tdo = torch.randn((S, H), generator=g, device="cuda").bfloat16()
+    o = torch.empty((S, H), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((nh, S), dtype=torch.float32, device="cuda")
+    T.attention_fwd(T.BF16, B, S, nh, dh, tq.data_ptr(), o.data_ptr(), lse.data_ptr())
+    dqkv = torch.empty_like(tq)
+    delta = torch.empty((nh, S), dtype=torch.float32, device="cuda")
+    dq_acc = torch.empty((S, H), dtype=torch.float32, device="cuda")
+    T.attention_bwd(T.BF16, B, S, nh, dh, tq.data_ptr(), o.data_ptr(), lse.data_ptr(), tdo.data_ptr(),
+                    dqkv.data_ptr(), delta.data_ptr(), dq_acc.data_ptr())
+    torch.cuda.synchronize()
+    # rows: first, tile edges, a ragged middle, the last; heads: first, middle, last
+    rows = [0, 1, 127, 128, 255, 4097, 16383, 20000, 32640, 32767]
+    got_o, ref_o, got_dq, ref_dq, errs_l = [], [], [], [], []
+    for h in (0, 13, 31):
+        k = tq[:, H + h * dh:H + (h + 1) * dh].double().cpu().numpy()
+        v = tq[:, 2 * H + h * dh:2 * H + (h + 1) * dh].double().cpu().numpy()
+        for i in rows:
+            qi = tq[i, h * dh:(h + 1) * dh].double().cpu().numpy()
+            doi = tdo[i, h * dh:(h + 1) * dh].double().cpu().numpy()
+            ro, rl, rdq = om.attention_row(i, qi, k, v, doi)
+            go = o[i, h * dh:(h + 1) * dh].double().cpu().numpy()
+            gdq = dqkv[i, h * dh:(h + 1) * dh].double().cpu().numpy()
+            got_o.append(go)
+            ref_o.append(ro)
+            got_dq.append(gdq)
+            ref_dq.append(rdq)   # row 0 attends to key 0 only: dq_0 = 0 exactly (scale = the sampled set's max)
+            errs_l.append(abs(float(lse[h, i]) - rl))
+    eo, edq = rel(np.array(got_o), np.array(ref_o)), rel(np.array(got_dq), np.array(ref_dq))
+    assert eo < 2e-2 and max(errs_l) < 1e-2 and edq < 3e-2, (eo, max(errs_l), edq)
+
+
+@pytest.mark.parametrize("M,N,K,a_k,b_k,f32", [(32768, 12288, 4096, True, True, False),      # QKV forward
+                                               (22016, 4096, 32768, False, False, True)])    # gate/up wgrad
+def test_gemm_full_size_sampled_elements(T, M, N, K, a_k, b_k, f32):
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = torch.randn((M, K) if a_k else (K, M), generator=g, device="cuda").bfloat16()
+    B = torch.randn((N, K) if b_k else (K, N), generator=g, device="cuda").bfloat16()
+    C = torch.full((M, N), 0.5, dtype=torch.float32 if f32 else torch.bfloat16, device="cuda")
+    T.gemm(T.BF16, M, N, K, A.data_ptr(), K if a_k else M, a_k, B.data_ptr(), K if b_k else N, b_k, C.data_ptr(), N,
+           c_f32=f32, accumulate=f32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7)
+    ms = np.concatenate([[0, M - 1, 127, 128, 255, 256], rng.integers(0, M, 58)])
+    ns = np.concatenate([[0, N - 1, 127, 128, 255, 256], rng.integers(0, N, 58)])
+    a_rows = (A[ms] if a_k else A[:, ms].t()).double().cpu().numpy()
+    b_rows = (B[ns] if b_k else B[:, ns].t()).double().cpu().numpy()
+    ref = np.einsum("ik,ik->i", a_rows, b_rows) + (0.5 if f32 else 0.0)
+    got = C[ms, ns].double().cpu().numpy()
+    err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
+    # fp32 output: the tensor core accumulates K = 32768 products in fp32; a random-walk rounding bound
+    # 4·sqrt(K)·2^-23 ≈ 8.6e-5 of the result's scale (measured 3.3e-5); bf16 output: one bf16 rounding
+    assert err < (4 * np.sqrt(K) * 2.0 ** -23 if f32 else 1e-2), err

@@ -240,6 +240,30 @@ def test_attention_closed_forms():
     np.testing.assert_allclose(P.sum(-1), 1.0, rtol=1e-14)
 
 
+def test_attention_row_form_equals_matrix_form_and_closed_forms():
+    """oracle.attention_row (full-size spot checks) agrees with the pinned matrix form row by row, and on its own
+    reproduces the closed forms: row 0 attends only to key 0 (o_0 = v_0, dq_0 = 0), a zero query gives the prefix
+    mean, and lse of a zero query is log(i + 1)."""
+    rng = np.random.default_rng(4)
+    S, nh, dh = 9, 2, 8
+    q, k, v, do = (rng.standard_normal((S, nh, dh)) for _ in range(4))
+    o, P = om.attention_fwd(q, k, v)
+    dq, _, _ = om.attention_bwd(do, q, k, v, o, P)
+    for h in range(nh):
+        for i in range(S):
+            oi, lse, dqi = om.attention_row(i, q[i, h], k[:, h], v[:, h], do[i, h])
+            np.testing.assert_allclose(oi, o[i, h], rtol=1e-12, atol=1e-14)
+            np.testing.assert_allclose(dqi, dq[i, h], rtol=1e-11, atol=1e-13)
+            s_ = (k[: i + 1, h] @ q[i, h]) / np.sqrt(dh)
+            assert abs(lse - np.log(np.sum(np.exp(s_)))) < 1e-12
+    o0, lse0, dq0 = om.attention_row(0, q[0, 0], k[:, 0], v[:, 0], do[0, 0])
+    np.testing.assert_allclose(o0, v[0, 0], rtol=1e-14)
+    np.testing.assert_allclose(dq0, 0.0, atol=1e-14)
+    oz, lz, _ = om.attention_row(5, np.zeros(dh), k[:, 0], v[:, 0], do[5, 0])
+    np.testing.assert_allclose(oz, v[:6, 0].mean(0), rtol=1e-13)
+    assert abs(lz - np.log(6)) < 1e-14
+
+
 def test_swiglu_closed_forms():
     u = np.linspace(-4, 4, 33)
     w = np.linspace(1, 2, 33)

@@ -1621,6 +1621,364 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+template <int DH>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+    fa_bwd6_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
+                  const __grid_constant__ CUtensorMap tmdq, const __grid_constant__ CUtensorMap tmdq64,
+                  const float* __restrict__ lse,
+                  const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
+                  float scale, float scale2, unsigned long long* __restrict__ trace) {
+  using L = BwdSmem<DH>;
+  // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
+  auto TR = [&](int it, int ev) {
+    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32) trace[it * 16 + ev] = clock64();
+  };
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *do_full = bar + 5, *do_empty = bar + 6,
+           *s_full = bar + 7, *dp_full = bar + 8, *tdp_free = bar + 9, *p_ready = bar + 10, *ds_ready = bar + 11,
+           *mm2_done = bar + 12, *dq_done = bar + 13, *stg_full = bar + 16, *peer_free = bar + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
+  float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
+
+  const int n_q = S / BQ;
+  // CTA pairs (cluster of 2) on key tiles 2p and 2p+1 of one head, heaviest pairs first: rank r = key tile 2p + r
+  const uint32_t rank = cluster_ctarank();
+  const int cl = static_cast<int>(blockIdx.x >> 1);
+  const int jt = 2 * (cl % (n_q / 2)) + static_cast<int>(rank);
+  const int h = cl / (n_q / 2);
+  const int b = blockIdx.y;
+  const int H = nh * DH;
+  const int row0 = b * S;
+  const int n_it = n_q - jt;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(sm) & 1023) __trap();  // SW128 tiles need a 1024-byte aligned base
+    tma_prefetch(&tm);
+    tma_prefetch(&tmdo);
+    tma_prefetch(&tmdq);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(do_full, 1);
+    mbar_init(do_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(tdp_free, 128);
+    mbar_init(p_ready, 128);
+    mbar_init(ds_ready, 128);
+    mbar_init(mm2_done, 1);
+    mbar_init(dq_done, 1);
+    mbar_init(stg_full, 64);   // the peer's 64 sender threads (one release.cluster arrive each)
+    mbar_init(peer_free, 1);   // the peer's reduce issuer: its staging buffer may be written
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();   // both CTAs' barriers initialised before any remote arrival
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * L::QB);
+      for (int a = 0; a < DH / 64; ++a) {
+        tma_load_2d(sm + L::OFF_K + a * ATOM, &tm, kv_full, H + h * DH + a * 64, row0 + jt * BQ);
+        tma_load_2d(sm + L::OFF_V + a * ATOM, &tm, kv_full, 2 * H + h * DH + a * 64, row0 + jt * BQ);
+      }
+      for (int it = 0; it < n_it; ++it) {
+        const int i = jt + it, st = it & 1;
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], L::QB + 1024);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_Q + st * L::QB + a * ATOM, &tm, &q_full[st], h * DH + a * 64, row0 + i * BQ);
+        const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ;
+        bulk_load(lse_s + st * 128, lse + li, 512, &q_full[st]);
+        bulk_load(del_s + st * 128, delta + li, 512, &q_full[st]);
+        mbar_wait(do_empty, (it & 1) ^ 1);
+        mbar_expect_tx(do_full, L::QB);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, do_full, h * DH + a * 64, row0 + i * BQ);
+      }
+    }
+  } else if (warp == 9) {
+    {  // whole warp (converged: descriptors stay uniform), one elected lane issues
+      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
+      constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
+      constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
+      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS),
+                     sDO = smem_u32(sm + L::OFF_DO);
+      auto issue_s = [&](int it) {  // Sᵀ_it = K·Q_itᵀ into tS
+        const int st = it & 1;
+        mbar_wait(&q_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          umma_f16_w(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
+        }
+        umma_commit_w(s_full);
+        TR(it, 0);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
+        mbar_wait(do_full, it & 1);
+        if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
+        TR(it, 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
+        umma_commit_w(dp_full);
+        mbar_wait(p_ready, it & 1);
+        TR(it, 2);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA_w(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
+        umma_commit_w(do_empty);
+        // Sᵀ_{it+1} right behind dV_it (same thread, in order: it overwrites Pᵀ_it only after dV_it has read it); the
+        // compute warps keep Pᵀ_it in registers for their dS pass, so Sᵀ_{it+1} is ready when that pass ends
+        if (it + 1 < n_it) issue_s(it + 1);
+        mbar_wait(ds_ready, it & 1);
+        TR(it, 3);
+        // dQ_it precedes dK_it: its drain (which frees the TMEM columns dPᵀ_{it+1} needs) overlaps dK_it
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
+        umma_commit_w(dq_done);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
+        umma_commit_w(&q_empty[st]);
+        umma_commit_w(mm2_done);
+      }
+    }
+  } else if (warp < 4) {
+    const int t = warp * 32 + lane;  // key row of the tile (TMEM lane)
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    uint8_t* sDS = sm + L::OFF_DS;
+    for (int it = 0; it < n_it; ++it) {
+      const int st = it & 1;
+      const float* ls = lse_s + st * 128;
+      const float* dl = del_s + st * 128;
+      mbar_wait(&q_full[st], (it >> 1) & 1);   // LSE_i, δ_i landed (bulk copies on the same barrier as Q_i)
+      mbar_wait(s_full, it & 1);
+      if (t == 0) TR(it, 4);
+      tc_fence_after();
+#pragma unroll
+      // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
+      uint32_t pk[4][16];   // Pᵀ_it, packed bf16, kept for the dS pass (Sᵀ_{it+1} overwrites its TMEM copy)
+      auto p_pass = [&](auto diag) {
+#pragma unroll
+        for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+          uint32_t uu[2][32];
+          tmem_ld32(tS + lane_off + cp * 32, uu[0]);
+          tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int c = cp + h2;
+            uint32_t (&pw)[16] = pk[c];
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
+              const float2 a2 = ffma2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
+                                      make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
+              float p0 = ex2(a2.x);
+              float p1 = ex2(a2.y);
+              if (decltype(diag)::value) {  // query index < key index is masked
+                if (c * 32 + k < t) p0 = 0.f;
+                if (c * 32 + k + 1 < t) p1 = 0.f;
+              }
+              pw[k / 2] = pack_bf16(p0, p1);
+            }
+            tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < cp*32+64)
+          }
+        }
+      };
+      if (it == 0)
+        p_pass(std::true_type{});
+      else
+        p_pass(std::false_type{});
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_ready);
+      if (t == 0) TR(it, 5);
+      mbar_wait(dp_full, it & 1);
+      if (t == 0) TR(it, 6);
+      if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ of the previous tile consumed by dK / dQ
+      if (t == 0) TR(it, 7);
+      tc_fence_after();
+#pragma unroll
+      for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+        uint32_t uu[2][32];
+        tmem_ld32(tdP + lane_off + cp * 32, uu[0]);
+        tmem_ld32(tdP + lane_off + cp * 32 + 32, uu[1]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = cp + h2;
+          const uint32_t (&pp)[16] = pk[c];
+          uint32_t d[16];
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            const float2 dl2 = *reinterpret_cast<const float2*>(dl + c * 32 + k);
+            const float2 ds2 = fmul2(make_float2(bf_lo(pp[k / 2]), bf_hi(pp[k / 2])),
+                                     fadd2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
+                                           make_float2(-dl2.x, -dl2.y)));
+            d[k / 2] = pack_bf16(ds2.x, ds2.y);
+          }
+          // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int chunk = (c & 1) * 4 + v;
+            *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
+                make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
+          }
+        }
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_ready);
+      if (t == 0) TR(it, 8);
+      if (lane == 0) TR(it, 12 + warp);   // per-warp dS done
+    }
+    // dK (× softmax scale) and dV rows of this key tile
+    mbar_wait(mm2_done, (n_it - 1) & 1);
+    tc_fence_after();
+    bf16* dkp = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + H + h * DH;
+    bf16* dvp = dkp + H;
+#pragma unroll 1
+    for (int c = 0; c < DH / 32; ++c) {
+      uint32_t u[32], w[32];
+      tmem_ld32(tdK + lane_off + c * 32, u);
+      tmem_ld32(tdV + lane_off + c * 32, w);
+      tmem_wait_ld();
+      uint4* k4 = reinterpret_cast<uint4*>(dkp + c * 32);
+      uint4* v4 = reinterpret_cast<uint4*>(dvp + c * 32);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        uint4 o, o2;
+        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * scale, __uint_as_float(u[8 * v + 1]) * scale);
+        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * scale, __uint_as_float(u[8 * v + 3]) * scale);
+        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * scale, __uint_as_float(u[8 * v + 5]) * scale);
+        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * scale, __uint_as_float(u[8 * v + 7]) * scale);
+        o2.x = pack_bf16(__uint_as_float(w[8 * v + 0]), __uint_as_float(w[8 * v + 1]));
+        o2.y = pack_bf16(__uint_as_float(w[8 * v + 2]), __uint_as_float(w[8 * v + 3]));
+        o2.z = pack_bf16(__uint_as_float(w[8 * v + 4]), __uint_as_float(w[8 * v + 5]));
+        o2.w = pack_bf16(__uint_as_float(w[8 * v + 6]), __uint_as_float(w[8 * v + 7]));
+        k4[v] = o;
+        v4[v] = o2;
+      }
+    }
+    tc_fence_before();
+  } else if (warp < 8) {
+    // dQ warps 4-7 (TMEM lane quarter warp % 4 = query rows 32q..32q+31 of dQ_i).  For the query tiles both CTAs of
+    // the pair visit (all but CTA 0's first), the two dQ_i partials are summed before the reduce-add into L2: CTA 0
+    // reduces rows 0-63, CTA 1 rows 64-127; the other half's owner receives the partner's rows into its staging
+    // buffer through distributed shared memory, adds its own and issues one 32 KB TMA reduce-add -- half the L2
+    // reduce traffic of unpaired CTAs.
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    uint8_t* stg = sm + L::OFF_STG;
+    const bool my_lo = q < 2;                          // this warp holds rows 0-63
+    const bool own = my_lo == (rank == 0);             // ... which this CTA reduces
+    const int r = t & 63;                              // row inside the half
+    const bool issuer = own && r == 0;                 // the thread that issues this CTA's half reduce
+    const uint32_t peer = rank ^ 1u;
+    int kk = 0;                                        // paired iterations so far
+    for (int it = 0; it < n_it; ++it) {
+      const int i = jt + it;
+      mbar_wait(dq_done, it & 1);    // dQ_i complete
+      tc_fence_after();
+      uint32_t u[DH / 32][32];
+#pragma unroll
+      for (int c = 0; c < DH / 32; ++c) tmem_ld32(tdP + lane_off + c * 32, u[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(tdp_free);                   // TMEM columns free for the next dPᵀ
+      if (rank == 0 && it == 0) {
+        // CTA 0's first query tile has no partner contribution: full 128-row reduce in two 64-column rounds
+#pragma unroll
+        for (int rd = 0; rd < DH / 64; ++rd) {
+          if (t == 0) bulk_wait_read0();
+          named_bar(2, 128);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              *reinterpret_cast<uint4*>(stg + hh * ATOM + t * 128 + ((jj ^ (t & 7)) << 4)) =
+                  make_uint4(u[rd * 2 + hh][4 * jj], u[rd * 2 + hh][4 * jj + 1], u[rd * 2 + hh][4 * jj + 2],
+                             u[rd * 2 + hh][4 * jj + 3]);
+          fence_async_smem();
+          named_bar(2, 128);
+          if (t == 0) {
+            tma_reduce_add_2d(&tmdq, stg, h * DH + rd * 64, row0 + i * BQ);
+            tma_reduce_add_2d(&tmdq, stg + ATOM, h * DH + rd * 64 + 32, row0 + i * BQ);
+            bulk_commit();
+          }
+        }
+        continue;
+      }
+      // paired query tile: staging layout = the half's 64 rows × DH fp32 as DH/32 boxes of (32 columns × 64 rows)
+      if (own) {
+        if (issuer) {                            // our staging buffer is read: the peer may write into it
+          bulk_wait_read0();
+          mbar_arrive_cluster(mapa_shared(peer_free, peer));
+        }
+        mbar_wait_cluster(stg_full, kk & 1);     // the peer's rows have landed
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c)
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            uint4* a = reinterpret_cast<uint4*>(stg + c * 8192 + r * 128 + ((jj ^ (r & 7)) << 4));
+            uint4 v = *a;
+            v.x = __float_as_uint(__uint_as_float(v.x) + __uint_as_float(u[c][4 * jj]));
+            v.y = __float_as_uint(__uint_as_float(v.y) + __uint_as_float(u[c][4 * jj + 1]));
+            v.z = __float_as_uint(__uint_as_float(v.z) + __uint_as_float(u[c][4 * jj + 2]));
+            v.w = __float_as_uint(__uint_as_float(v.w) + __uint_as_float(u[c][4 * jj + 3]));
+            *a = v;
+          }
+        fence_async_smem();
+        named_bar(3, 64);
+        if (issuer) {
+#pragma unroll
+          for (int c = 0; c < DH / 32; ++c)
+            tma_reduce_add_2d(&tmdq64, stg + c * 8192, h * DH + c * 32, row0 + i * BQ + (rank == 0 ? 0 : 64));
+          bulk_commit();
+        }
+      } else {
+        mbar_wait(peer_free, kk & 1);            // the peer's staging buffer may be written
+        const uint32_t base = mapa_shared(stg, peer);
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c)
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            st_cluster_v4(base + c * 8192 + r * 128 + ((jj ^ (r & 7)) << 4), u[c][4 * jj], u[c][4 * jj + 1],
+                          u[c][4 * jj + 2], u[c][4 * jj + 3]);
+        mbar_arrive_cluster(mapa_shared(stg_full, peer));
+      }
+      ++kk;
+    }
+    if (t == 0 || issuer) bulk_wait_all0();
+  }
+  tc_fence_before();
+  cluster_sync();   // the peer's remote arrivals and staging writes are done before either CTA exits
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+
 // δ_i = Σ_d dO_id·O_id ; one warp per (row, head)
 __global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16* __restrict__ o,
                                 const bf16* __restrict__ dout, float* __restrict__ delta,
@@ -1825,7 +2183,20 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
     }
     return p;
   }();
-  if (dh == 128) {
+  static const int bwd_ver = [] {
+    const char* e = std::getenv("TAWPIPE_FA_BWD");
+    return e ? std::atoi(e) : 5;
+  }();
+  if (dh == 128 && bwd_ver == 6 && (S / BQ) % 2 == 0) {
+    // v6 (experimental, off by default): CTA pairs summing their dQ partials through distributed shared memory
+    // (half the L2 reduce traffic).  Correct, but measured 2× slower at C3: with one staging buffer per CTA the
+    // per-tile exchange couples the two CTAs' pipelines so that they alternate instead of overlapping.
+    CUtensorMap tmdq64 = make_tmap_f32_2d(dq_acc, H, rows, H, 64);
+    static bool once = (prep(fa_bwd6_kernel<128>, BwdSmem<128>::BYTES), true);
+    (void)once;
+    fa_bwd6_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, tmdq64, lse2, delta, dq_acc, dqkv, S,
+                                                                nh, scale, scale2, trace);
+  } else if (dh == 128) {
     static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
     (void)once;
     fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,

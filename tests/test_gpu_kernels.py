@@ -212,3 +212,24 @@ def test_gemm_full_size_sampled_elements(T, M, N, K, a_k, b_k, f32):
     # fp32 output: the tensor core accumulates K = 32768 products in fp32; a random-walk rounding bound
     # 4·sqrt(K)·2^-23 ≈ 8.6e-5 of the result's scale (measured 3.3e-5); bf16 output: one bf16 rounding
     assert err < (4 * np.sqrt(K) * 2.0 ** -23 if f32 else 1e-2), err
+
+
+def test_attention_bwd_cta_pair_variant_matches_oracle():
+    """The experimental CTA-pair backward (TAWPIPE_FA_BWD=6: dQ partials of two key tiles summed through
+    distributed shared memory before the reduce-add) against the oracle, in a fresh process (the variant is
+    chosen once per process)."""
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    code = ("import sys; sys.path.insert(0, 'tests'); import torch; import test_gpu_kernels as t; "
+            "from paper_2511_09741_b200 import tawpipe as T; T.lib(); "
+            "tq, tdo = t.attn_case(1, 1024, 2, 128, 12, torch.bfloat16); "
+            "o, lse, d = t.run_attention(T, T.BF16, tq, tdo, 1, 1024, 2, 128); "
+            "ro, rl, rd = t.oracle_attention(tq, tdo, 1, 1024, 2, 128); "
+            "assert t.rel(d, rd) < 3e-2, t.rel(d, rd); print('ok')")
+    import os
+    env = dict(os.environ, TAWPIPE_FA_BWD="6")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

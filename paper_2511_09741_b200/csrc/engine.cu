@@ -1168,7 +1168,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   }
   c.dhb.resize(m);
   for (auto& p : c.dhb) p = dmalloc(T * H * esz);
-  c.dY = dmalloc(T * I * esz);
+  if (!c.bf || gemm_force_simt()) c.dY = dmalloc(T * I * esz);   // the tcgen05 path fuses SwiGLU' into the dgrad
   c.dGU = dmalloc(T * 2 * I * esz);
   c.db = dmalloc(T * H * esz);
   c.dh1 = dmalloc(T * H * esz);
@@ -1211,7 +1211,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   if (d->ckpt == 1) {
     size_t fr = 0, tot = 0;
     TP_CUDA(cudaMemGetInfo(&fr, &tot));
-    const size_t margin = size_t(6) << 30;   // NCCL channels, allocator slack
+    const size_t margin = size_t(P > 1 ? 6 : 3) << 30;   // NCCL channels (none at P = 1), allocator slack
     size_t budget = fr > margin ? fr - margin : 0;
     if (const char* e = std::getenv("TAWPIPE_KEEP_BUDGET_KB")) budget = std::min(budget, size_t(std::atoll(e)) << 10);
     const size_t n = static_cast<size_t>(L) * m, TT = static_cast<size_t>(T);

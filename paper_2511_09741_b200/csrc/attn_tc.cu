@@ -800,12 +800,17 @@ __global__ void __launch_bounds__(224, 1)
 // ----------------------------------------------------------------------------------------------- forward v5
 // Two query tiles per CTA (A = 2p+1, B = 2p: the same K/V stream, A one key tile longer) with one softmax
 // warpgroup each, so that one tile's exponentials run on the MUFU while the other tile's scores are loaded,
-// reduced and written back (ping-pong across tiles instead of within one).  Each tile has one S/P buffer and one
+// reduced and written back, and each tile's P·V / next S run on the tensor core under the other tile's softmax.  Each tile has one S/P buffer and one
 // O accumulator in TMEM (4 × 128 columns); S_t(j) is issued right behind P·V_t(j−1) by the same thread, so its
 // completion implies P·V_t(j−1)'s: O_t is stable whenever softmax t runs and the lazy rescale never waits.
 //   warps 0-3: softmax of tile A, warps 4-7: softmax of tile B (thread = row, lane quarter = warp % 4)
 //   warp 8: MMA issuer (P·V_t(j) then S_t(j+1), in order), warp 9: TMA producer (Q_A, Q_B once; K, V 2-stage rings)
 //   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
+// Strict alternation of the two tiles' exponential passes (named-barrier ping-pong): measured 3-4 % slower than
+// letting both warpgroups run freely (two warps per SMSP keep the MUFU busier than one warp alternating), so off.
+#ifndef FWD5_PINGPONG
+#define FWD5_PINGPONG 0
+#endif
 template <int DH>
 struct Fwd5Smem {
   static constexpr int QB = DH / 64 * ATOM;
@@ -991,10 +996,12 @@ __global__ void __launch_bounds__(384, 1)
       }
       // ping-pong: the two tiles take turns on the exponential pass (A_j, B_j, A_{j+1}, ...), so that one tile's
       // loads / max / rescale / P store overlap the other tile's MUFU work (named barriers 1: A may go, 2: B may go)
-      if (t == 0) {
-        if (j > 0) named_bar(1, 256);
-      } else {
-        named_bar(2, 256);
+      if (FWD5_PINGPONG) {
+        if (t == 0) {
+          if (j > 0) named_bar(1, 256);
+        } else {
+          named_bar(2, 256);
+        }
       }
       if (r == 0) TR(j, 3 * t + 1);
       float2 sa2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -1012,10 +1019,12 @@ __global__ void __launch_bounds__(384, 1)
         tmem_st16(tS + c * 16, pw);
       }
       if (r == 0) TR(j, 3 * t + 2);
-      if (t == 0) {
-        if (j < n_kv - 1) named_bar_arrive(2, 256);   // B's step j (tile B has n_kv − 1 steps)
-      } else {
-        named_bar_arrive(1, 256);                     // A's step j + 1
+      if (FWD5_PINGPONG) {
+        if (t == 0) {
+          if (j < n_kv - 1) named_bar_arrive(2, 256);   // B's step j (tile B has n_kv − 1 steps)
+        } else {
+          named_bar_arrive(1, 256);                     // A's step j + 1
+        }
       }
       const float2 t2 = fadd2(fadd2(sa2[0], sa2[1]), fadd2(sa2[2], sa2[3]));
       l += t2.x + t2.y;

@@ -142,7 +142,7 @@ def test_attention_fp32_matches_oracle(T, B, S, nh, dh):
 
 
 @pytest.mark.parametrize("B,S,nh,dh", [(1, 128, 2, 64), (1, 384, 2, 128), (2, 256, 3, 128), (1, 1024, 1, 128),
-                                      (1, 4096, 2, 128)])
+                                      (1, 4096, 2, 128), (2, 512, 2, 64)])   # odd / even query-tile counts, d_h 64
 def test_attention_bf16_matches_oracle(T, B, S, nh, dh):
     tq, tdo = attn_case(B, S, nh, dh, 12, torch.bfloat16)
     o, lse, dqkv = run_attention(T, T.BF16, tq, tdo, B, S, nh, dh)

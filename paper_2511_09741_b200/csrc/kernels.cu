@@ -483,6 +483,71 @@ __global__ void rmsnorm_bwd_dx_v8_kernel(const bf16* __restrict__ dy, const bf16
   }
 }
 
+// ---- CTA-per-row forms for large H (H = THREADS·8·NVT): each thread keeps NVT 8-wide vectors in registers and
+// the row statistic is a block reduction; the warp-per-row forms above need H/32 values per thread, which for
+// H ≥ 2048 spills (H = 4096: 255 registers + 592 B of stack for the backward)
+template <int THREADS, int NVT>
+__global__ void __launch_bounds__(THREADS) rmsnorm_fwd_row_kernel(const bf16* __restrict__ x, const bf16* __restrict__ g,
+                                                                  bf16* __restrict__ y, float* __restrict__ rstd,
+                                                                  int H, float eps) {
+  __shared__ float sh[THREADS / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * H;
+  float xv[NVT][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NVT; ++i) {
+    ld8(x + base + (i * THREADS + threadIdx.x) * 8, xv[i]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss += xv[i][k] * xv[i][k];
+  }
+  const float r = rsqrtf(block_sum<THREADS>(ss, sh) / H + eps);
+#pragma unroll
+  for (int i = 0; i < NVT; ++i) {
+    float gv[8], o[8];
+    ld8(g + (i * THREADS + threadIdx.x) * 8, gv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = xv[i][k] * r * gv[k];
+    st8(y + base + (i * THREADS + threadIdx.x) * 8, o);
+  }
+  if (threadIdx.x == 0) rstd[blockIdx.x] = r;
+}
+
+// dx = r·(dy⊙g) − x·(r³/H)·Σ(dy⊙g⊙x) (+ res)
+template <int THREADS, int NVT>
+__global__ void __launch_bounds__(THREADS) rmsnorm_bwd_dx_row_kernel(const bf16* __restrict__ dy,
+                                                                     const bf16* __restrict__ x,
+                                                                     const bf16* __restrict__ g,
+                                                                     const float* __restrict__ rstd,
+                                                                     const bf16* __restrict__ res,
+                                                                     bf16* __restrict__ dx, int H) {
+  __shared__ float sh[THREADS / 32];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * H;
+  const float r = rstd[blockIdx.x];
+  float dg[NVT][8], xv[NVT][8];
+  float dot = 0.f;
+#pragma unroll
+  for (int i = 0; i < NVT; ++i) {
+    float gv[8];
+    ld8(dy + base + (i * THREADS + threadIdx.x) * 8, dg[i]);
+    ld8(x + base + (i * THREADS + threadIdx.x) * 8, xv[i]);
+    ld8(g + (i * THREADS + threadIdx.x) * 8, gv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      dg[i][k] *= gv[k];
+      dot += dg[i][k] * xv[i][k];
+    }
+  }
+  const float coef = r * r * r * block_sum<THREADS>(dot, sh) / H;
+#pragma unroll
+  for (int i = 0; i < NVT; ++i) {
+    float o[8], rs[8];
+    if (res) ld8(res + base + (i * THREADS + threadIdx.x) * 8, rs);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = r * dg[i][k] - xv[i][k] * coef + (res ? rs[k] : 0.f);
+    st8(dx + base + (i * THREADS + threadIdx.x) * 8, o);
+  }
+}
+
 // dγ_c += Σ_rows dy_rc · x_rc · r_r : block = 8 warps over a 256-column block and a 256-row chunk
 __global__ void rmsnorm_dgamma_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
                                          const float* __restrict__ rstd, float* __restrict__ dg_acc, int64_t rows,
@@ -538,9 +603,18 @@ void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H,
     switch (H) {
       case 256: rmsnorm_fwd_v8_kernel<1><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
       case 1024: rmsnorm_fwd_v8_kernel<4><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
-      case 2048: rmsnorm_fwd_v8_kernel<8><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
-      case 4096: rmsnorm_fwd_v8_kernel<16><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
-      case 5120: rmsnorm_fwd_v8_kernel<20><<<blocks, 256, 0, s>>>(x, g, y, rstd, rows, H, eps); LAUNCHED(); return;
+      case 2048:
+        rmsnorm_fwd_row_kernel<256, 1><<<static_cast<unsigned>(rows), 256, 0, s>>>(x, g, y, rstd, H, eps);
+        LAUNCHED();
+        return;
+      case 4096:
+        rmsnorm_fwd_row_kernel<256, 2><<<static_cast<unsigned>(rows), 256, 0, s>>>(x, g, y, rstd, H, eps);
+        LAUNCHED();
+        return;
+      case 5120:
+        rmsnorm_fwd_row_kernel<128, 5><<<static_cast<unsigned>(rows), 128, 0, s>>>(x, g, y, rstd, H, eps);
+        LAUNCHED();
+        return;
       default: break;
     }
   }
@@ -556,9 +630,15 @@ void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T
       switch (H) {
         case 256: rmsnorm_bwd_dx_v8_kernel<1><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
         case 1024: rmsnorm_bwd_dx_v8_kernel<4><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
-        case 2048: rmsnorm_bwd_dx_v8_kernel<8><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
-        case 4096: rmsnorm_bwd_dx_v8_kernel<16><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
-        default: rmsnorm_bwd_dx_v8_kernel<20><<<blocks, 256, 0, s>>>(dy, x, g, rstd, res, dx, rows, H); break;
+        case 2048:
+          rmsnorm_bwd_dx_row_kernel<256, 1><<<static_cast<unsigned>(rows), 256, 0, s>>>(dy, x, g, rstd, res, dx, H);
+          break;
+        case 4096:
+          rmsnorm_bwd_dx_row_kernel<256, 2><<<static_cast<unsigned>(rows), 256, 0, s>>>(dy, x, g, rstd, res, dx, H);
+          break;
+        default:
+          rmsnorm_bwd_dx_row_kernel<128, 5><<<static_cast<unsigned>(rows), 128, 0, s>>>(dy, x, g, rstd, res, dx, H);
+          break;
       }
       LAUNCHED();
       rmsnorm_dgamma_v8_kernel<<<dim3(H / 256, static_cast<unsigned>((rows + 255) / 256)), 256, 0, s>>>(

@@ -2246,6 +2246,36 @@ __global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16*
   }
 }
 
+// δ with 16-byte loads: one block per row, each thread 32 consecutive features (4 × 8 bf16) of one head,
+// dh/32 threads per head reduced with shuffles (d_h ∈ {64, 128}: 2 or 4 lanes)
+__global__ void fa_delta_v8_kernel(int S, int nh, int dh, const bf16* __restrict__ o, const bf16* __restrict__ dout,
+                                   float* __restrict__ delta, const float* __restrict__ lse, float* __restrict__ lse2) {
+  const int64_t row = blockIdx.x;
+  const int H = nh * dh;
+  const int64_t base = row * H + static_cast<int64_t>(threadIdx.x) * 32;
+  float acc = 0.f;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const uint4 a = *reinterpret_cast<const uint4*>(o + base + v * 8);
+    const uint4 c = *reinterpret_cast<const uint4*>(dout + base + v * 8);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 fa = __bfloat1622float2(a2[i]), fc = __bfloat1622float2(c2[i]);
+      acc += fa.x * fc.x + fa.y * fc.y;
+    }
+  }
+  const int per_head = dh / 32;
+  for (int sft = 1; sft < per_head; sft <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sft);
+  if (threadIdx.x % per_head == 0) {
+    const int h = threadIdx.x / per_head;
+    const int64_t li = (row / S * nh + h) * S + row % S;
+    delta[li] = acc;
+    lse2[li] = lse[li] * LOG2E;   // log2-domain LSE for the exp2 of the backward
+  }
+}
+
 // dq (bf16, × softmax scale) <- fp32 accumulator
 __global__ void fa_dq_convert_kernel(int64_t rows, int H, const float* __restrict__ acc, bf16* __restrict__ dqkv,
                                      float scale) {
@@ -2423,8 +2453,11 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
     TP_CUDA(cudaMalloc(&lse2, rows * nh * sizeof(float)));
     lse2_n = rows * nh;
   }
-  fa_delta_kernel<<<static_cast<unsigned>((rows * nh * 32 + 255) / 256), 256, 0, s>>>(rows, S, nh, dh, o, dout,
-                                                                                    delta, lse, lse2);
+  if (H % 32 == 0 && H / 32 <= 1024 && (dh == 64 || dh == 128))
+    fa_delta_v8_kernel<<<static_cast<unsigned>(rows), H / 32, 0, s>>>(S, nh, dh, o, dout, delta, lse, lse2);
+  else
+    fa_delta_kernel<<<static_cast<unsigned>((rows * nh * 32 + 255) / 256), 256, 0, s>>>(rows, S, nh, dh, o, dout,
+                                                                                      delta, lse, lse2);
   TP_CUDA(cudaMemsetAsync(dq_acc, 0, rows * H * sizeof(float), s));
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, rows, 3ll * H, 128);
   CUtensorMap tmdo = make_tmap_bf16_2d(dout, H, rows, H, 128);

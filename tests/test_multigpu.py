@@ -64,7 +64,11 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
            "--cfg", json.dumps(dict(base, n_layers=L)), "--G", str(G), "--N", str(N), "--steps", str(steps),
            "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else []) \
         + (["--ring"] if ring else []) + (["--literal"] if literal else []) + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    for _ in range(3):   # the free port can be taken between probing and torchrun's bind: retry on EADDRINUSE
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
+        cmd[cmd.index(next(c for c in cmd if c.startswith("--master-port=")))] = f"--master-port={free_port()}"
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
     # oracle: plain single-device step on the same tokens

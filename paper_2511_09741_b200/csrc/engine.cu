@@ -65,13 +65,14 @@ struct Acts {  // one (layer, micro-batch) forward's saved tensors
 //   KEEP_ATTN  attention output O and LSE       (recompute skips the attention forward)
 //   KEEP_QKV   post-RoPE q|k|v                   (skips the QKV GEMM and RoPE)
 //   KEEP_H1    h1 = h + O·Woᵀ                    (skips the O GEMM)
-//   KEEP_MLP   gu = [x·Wgateᵀ | x·Wupᵀ] and y     (skips the gate/up GEMM + SwiGLU)
+//   KEEP_MLP   gu = [x·Wgateᵀ | x·Wupᵀ]            (skips the gate/up GEMM; y = SwiGLU(gu) is re-derived by the
+//                                                 elementwise kernel: 1.4 GB kept per layer instead of 2.2)
 // The two RMSNorms are always recomputed (cheap; their outputs and 1/rms feed the backward).  A kept tensor is
 // the output of the same kernel on the same inputs as its recompute would be: results are bit-identical.
 enum : uint8_t { KEEP_ATTN = 1, KEEP_QKV = 2, KEEP_H1 = 4, KEEP_MLP = 8 };
 struct Kept {
   uint8_t flags = 0;
-  void *o = nullptr, *qkv = nullptr, *h1 = nullptr, *gu = nullptr, *y = nullptr;
+  void *o = nullptr, *qkv = nullptr, *h1 = nullptr, *gu = nullptr;
   float* lse = nullptr;
 };
 
@@ -625,10 +626,7 @@ View view(int l, int mb) {
     }
     if (k.flags & KEEP_QKV) v.qkv = k.qkv;
     if (k.flags & KEEP_H1) v.h1 = k.h1;
-    if (k.flags & KEEP_MLP) {
-      v.gu = k.gu;
-      v.y = k.y;
-    }
+    if (k.flags & KEEP_MLP) v.gu = k.gu;   // y stays in the scratch set (re-derived from gu in the recompute)
   }
   return v;
 }
@@ -678,6 +676,10 @@ void layer_forward(int l, int mb, void* W, bool write_out) {
       BY_TYPE(swiglu_fwd<float>((const float*)A.gu, (float*)A.y, T, (int)I, s),
               swiglu_fwd<bf16>((const bf16*)A.gu, (bf16*)A.y, T, (int)I, s));
     }
+  } else {   // recompute with a kept gu: y = SwiGLU(gu) for the down projection's wgrad
+    Timed t(s, 4, 0);
+    BY_TYPE(swiglu_fwd<float>((const float*)A.gu, (float*)A.y, T, (int)I, s),
+            swiglu_fwd<bf16>((const bf16*)A.gu, (bf16*)A.y, T, (int)I, s));
   }
   if (write_out) gemm(T, H, I, A.y, I, true, w.wdown, I, true, ck(l + 1, mb), H, false, false, A.h1, s);
   if (!write_out) g->recompute_gflop += work * 1e-9;
@@ -1215,7 +1217,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
     size_t budget = fr > margin ? fr - margin : 0;
     if (const char* e = std::getenv("TAWPIPE_KEEP_BUDGET_KB")) budget = std::min(budget, size_t(std::atoll(e)) << 10);
     const size_t n = static_cast<size_t>(L) * m, TT = static_cast<size_t>(T);
-    const size_t cost[4] = {TT * H * esz + TT * c.nh * 4, TT * 3 * H * esz, TT * H * esz, TT * 3 * I * esz};
+    const size_t cost[4] = {TT * H * esz + TT * c.nh * 4, TT * 3 * H * esz, TT * H * esz, TT * 2 * I * esz};
     c.kept.assign(n, Kept{});
     for (int lv = 0; lv < 4; ++lv) {
       const size_t cnt = std::min(n, budget / cost[lv]);
@@ -1225,7 +1227,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
           case 0: k.o = dmalloc(TT * H * esz); k.lse = (float*)dmalloc(TT * c.nh * 4); break;
           case 1: k.qkv = dmalloc(TT * 3 * H * esz); break;
           case 2: k.h1 = dmalloc(TT * H * esz); break;
-          case 3: k.gu = dmalloc(TT * 2 * I * esz); k.y = dmalloc(TT * I * esz); break;
+          case 3: k.gu = dmalloc(TT * 2 * I * esz); break;
         }
         k.flags |= static_cast<uint8_t>(1u << lv);
       }

@@ -68,7 +68,9 @@ struct Acts {  // one (layer, micro-batch) forward's saved tensors
 //   KEEP_MLP   gu = [x·Wgateᵀ | x·Wupᵀ]            (skips the gate/up GEMM; y = SwiGLU(gu) is re-derived by the
 //                                                 elementwise kernel: 1.4 GB kept per layer instead of 2.2)
 // The two RMSNorms are always recomputed (cheap; their outputs and 1/rms feed the backward).  A kept tensor is
-// the output of the same kernel on the same inputs as its recompute would be: results are bit-identical.
+// the output of the same kernel on the same inputs as its recompute would be, so results are bit-identical, except
+// y at the MLP level: re-derived from the bf16 gu rather than the GEMM epilogue's fp32 accumulators (one bf16
+// rounding apart).
 enum : uint8_t { KEEP_ATTN = 1, KEEP_QKV = 2, KEEP_H1 = 4, KEEP_MLP = 8 };
 struct Kept {
   uint8_t flags = 0;

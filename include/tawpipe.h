@@ -74,8 +74,9 @@ typedef struct tawpipe_dims {
   int32_t ckpt;          /* activation checkpointing: 0 none (all activations kept);
                           * 1 keep each layer's input h_l and recompute the layer in backward, but
                           * keep more of it while device memory allows (selective: attention O+LSE,
-                          * then q|k|v, then h1, then the MLP's gu and y, per (layer, micro-batch);
-                          * the recompute skips what was kept; results are bit-identical);
+                          * then q|k|v, then h1, then the MLP's gu, per (layer, micro-batch); the
+                          * recompute skips what was kept; results are bit-identical except the
+                          * MLP's y, re-derived from the kept bf16 gu: one bf16 rounding apart);
                           * 2 keep h_l only (full recompute)                                      */
   int32_t schedule;      /* TAWPIPE_GWPS, TAWPIPE_RING or TAWPIPE_LITERAL, optionally | TAWPIPE_NO_CCO */
   int32_t reserved;      /* must be 0                                                            */

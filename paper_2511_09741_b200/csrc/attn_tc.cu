@@ -1068,7 +1068,8 @@ __global__ void __launch_bounds__(384, 1)
 // goes back over the first 32 columns of its half, P·V_t(j, half) is a K = 64 MMA, and S_t(j+1, half) is issued
 // right behind it.  A tile's softmax therefore works on one half while the tensor core runs the other half's P·V
 // and next S, instead of waiting for a whole P·V + S after each 128-key step (measured ≈2,050 cycles per step in
-// v5).  Sustained at S = 32K, 32 heads: 7.9 ms against v5's 8.35 ms.
+// v5).  One issuer warp per tile keeps the two tiles' MMA streams independent.  Sustained at S = 32K, 32 heads:
+// 7.35 ms against v5's 8.4 ms (7.9 ms with a single in-order issuer for both tiles).
 //   TMEM per tile t: S/P [128t, 128t+128) as halves of 64 columns, O_t [256+128t, 384+128t)
 template <int DH>
 __global__ void __launch_bounds__(384, 1)
@@ -1101,9 +1102,9 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(q_full, 1);
     for (int i = 0; i < NST; ++i) {
       mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+      mbar_init(&k_empty[i], 2);   // released by both tiles' issuers (the last K / V only by tile A's: not reused)
       mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
+      mbar_init(&v_empty[i], 2);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
@@ -1113,7 +1114,7 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(&o_done[1], 1);
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc(tmem_slot, 512);
+  if (warp == 8) tmem_alloc(tmem_slot, 512);   // warps 0-7 softmax, 8 / 10 issuers, 9 producer
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1140,12 +1141,16 @@ __global__ void __launch_bounds__(384, 1)
                       row0 + j * BQ);
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == 8 || warp == 10) {
+    // one in-order issuer per tile (warp 8: A on SMSP 0, warp 10: B on SMSP 2): P·V_t(j, half) then S_t(j+1, half),
+    // so that a tile's MMAs never queue behind the other tile's softmax
+    const int t = warp == 8 ? 0 : 1;
+    const int n_kv_t = n_kv_A - t;
     constexpr uint32_t id_qk = umma_idesc_bf16(128, 64, false, false);
     constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
-    auto issue_s = [&](int t, int jj, int hf) {   // S_t(jj, hf) = Q_t · K_jj[64·hf .. 64·hf+63]ᵀ (N = 64)
+    const uint32_t sQ = smem_u32(sm + L::OFF_Q + t * L::QB);
+    auto issue_s = [&](int jj, int hf) {   // S_t(jj, hf) = Q_t · K_jj[64·hf .. 64·hf+63]ᵀ (N = 64)
       const uint32_t sK = smem_u32(sm + L::OFF_K + (jj % NST) * L::QB) + hf * 8192;
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q + t * L::QB);
 #pragma unroll
       for (int ks = 0; ks < DH / 16; ++ks)
         umma_f16_w(tmem + t * 128 + hf * 64, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
@@ -1154,29 +1159,25 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(q_full, 0);
     mbar_wait(&k_full[0], 0);
     tc_fence_after();
-    for (int hf = 0; hf < 2; ++hf)
-      for (int t = 0; t < 2; ++t) issue_s(t, 0, hf);
+    issue_s(0, 0);
+    issue_s(0, 1);
     umma_commit_w(&k_empty[0]);
-    for (int j = 0; j < n_kv_A; ++j) {
+    for (int j = 0; j < n_kv_t; ++j) {
       const int st = j % NST;
       mbar_wait(&v_full[st], (j / NST) & 1);
       const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
-      const bool next = j + 1 < n_kv_A;
+      const bool next = j + 1 < n_kv_t;
       if (next) mbar_wait(&k_full[(j + 1) % NST], ((j + 1) / NST) & 1);
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
+        mbar_wait(&p_ready[t * 2 + hf], j & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (j >= n_kv_A - t) continue;   // tile B has one key tile fewer
-          mbar_wait(&p_ready[t * 2 + hf], j & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)   // keys 64·hf + 16·ks: P packed over the half's first 32 columns
-            umma_f16_tmemA_w(tmem + 256 + t * 128, tmem + t * 128 + hf * 64 + ks * 8, desc_mn(sV, hf * 4 + ks), id_pv,
-                             (j | hf | ks) > 0);
-          umma_commit_w(&o_done[t]);
-          if (j + 1 < n_kv_A - t) issue_s(t, j + 1, hf);
-        }
+        for (int ks = 0; ks < 4; ++ks)   // keys 64·hf + 16·ks: P packed over the half's first 32 columns
+          umma_f16_tmemA_w(tmem + 256 + t * 128, tmem + t * 128 + hf * 64 + ks * 8, desc_mn(sV, hf * 4 + ks), id_pv,
+                           (j | hf | ks) > 0);
+        umma_commit_w(&o_done[t]);
+        if (next) issue_s(j + 1, hf);
       }
       umma_commit_w(&v_empty[st]);
       if (next) umma_commit_w(&k_empty[(j + 1) % NST]);
@@ -2325,11 +2326,11 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
     if (dh == 128) {
       static bool once = (prep(fa_fwd7_kernel<128>, Fwd5Smem<128>::BYTES), true);
       (void)once;
-      fa_fwd7_kernel<128><<<grid7, 320, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+      fa_fwd7_kernel<128><<<grid7, 352, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
     } else {
       static bool once = (prep(fa_fwd7_kernel<64>, Fwd5Smem<64>::BYTES), true);
       (void)once;
-      fa_fwd7_kernel<64><<<grid7, 320, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+      fa_fwd7_kernel<64><<<grid7, 352, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
     }
     TP_CUDA(cudaGetLastError());
     g_kstats.launches++;

@@ -1681,12 +1681,12 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA_w(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
         umma_commit_w(do_empty);
+        // Sᵀ_{it+1} right behind dV_it (same thread, in order: it overwrites Pᵀ_it only after dV_it has read it); the
+        // compute warps keep Pᵀ_it in registers for their dS pass, so Sᵀ_{it+1} is ready when that pass ends
+        if (it + 1 < n_it) issue_s(it + 1);
         mbar_wait(ds_ready, it & 1);
         TR(it, 3);
-        // Pᵀ_it fully consumed (dV issued before, dS pass done): Sᵀ_{it+1} goes first so that the softmax warps
-        // compute Pᵀ_{it+1} while dQ_it and dK_it run on the tensor core.  dQ_it precedes dK_it: its drain (which
-        // frees the TMEM columns dPᵀ_{it+1} needs) then overlaps dK_it instead of following it
-        if (it + 1 < n_it) issue_s(it + 1);
+        // dQ_it precedes dK_it: its drain (which frees the TMEM columns dPᵀ_{it+1} needs) overlaps dK_it
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
@@ -1711,6 +1711,7 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
 #pragma unroll
       // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
+      uint32_t pk[4][16];   // Pᵀ_it, packed bf16, kept for the dS pass (Sᵀ_{it+1} overwrites its TMEM copy)
       auto p_pass = [&](auto diag) {
 #pragma unroll
         for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
@@ -1721,7 +1722,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             const int c = cp + h2;
-            uint32_t pw[16];
+            uint32_t (&pw)[16] = pk[c];
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
               const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
@@ -1754,20 +1755,19 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
 #pragma unroll
       for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
-        uint32_t uu[2][32], pp[2][16];
+        uint32_t uu[2][32];
         tmem_ld32(tdP + lane_off + cp * 32, uu[0]);
         tmem_ld32(tdP + lane_off + cp * 32 + 32, uu[1]);
-        tmem_ld16(tS + lane_off + cp * 16, pp[0]);
-        tmem_ld16(tS + lane_off + cp * 16 + 16, pp[1]);
         tmem_wait_ld();
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2) {
           const int c = cp + h2;
+          const uint32_t (&pp)[16] = pk[c];
           uint32_t d[16];
 #pragma unroll
           for (int k = 0; k < 32; k += 2) {
             const float2 dl2 = *reinterpret_cast<const float2*>(dl + c * 32 + k);
-            const float2 ds2 = fmul2(make_float2(bf_lo(pp[h2][k / 2]), bf_hi(pp[h2][k / 2])),
+            const float2 ds2 = fmul2(make_float2(bf_lo(pp[k / 2]), bf_hi(pp[k / 2])),
                                      fadd2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
                                            make_float2(-dl2.x, -dl2.y)));
             d[k / 2] = pack_bf16(ds2.x, ds2.y);
@@ -1822,6 +1822,7 @@ __global__ void __launch_bounds__(320, 1)
     const int t = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     uint8_t* stg = sm + L::OFF_STG;
+    int rnd = 0;   // staging rounds issued so far (buffer half = rnd & 1)
     for (int it = 0; it < n_it; ++it) {
       const int i = jt + it;
       mbar_wait(dq_done, it & 1);    // dQ_i complete
@@ -1834,22 +1835,21 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       mbar_arrive(tdp_free);                   // TMEM columns free for the next dPᵀ
       if (t == 0) TR(it, 10);
+      // 32-column rounds through the two 16 KB halves of the staging buffer: a round waits only for the reduce
+      // issued two rounds earlier (wait_group.read 1), so writing one half overlaps the TMA read of the other
 #pragma unroll
-      for (int rd = 0; rd < DH / 64; ++rd) {
-        if (t == 0) bulk_wait_read0();         // staging buffer read by the previous reduce
+      for (int c = 0; c < DH / 32; ++c, ++rnd) {
+        uint8_t* buf = stg + (rnd & 1) * ATOM;
+        if (t == 0) bulk_wait_read1();
         named_bar(2, 128);
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<uint4*>(stg + hh * ATOM + t * 128 + ((j ^ (t & 7)) << 4)) =
-                make_uint4(u[rd * 2 + hh][4 * j], u[rd * 2 + hh][4 * j + 1], u[rd * 2 + hh][4 * j + 2],
-                           u[rd * 2 + hh][4 * j + 3]);
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<uint4*>(buf + t * 128 + ((j ^ (t & 7)) << 4)) =
+              make_uint4(u[c][4 * j], u[c][4 * j + 1], u[c][4 * j + 2], u[c][4 * j + 3]);
         fence_async_smem();
         named_bar(2, 128);
         if (t == 0) {
-          tma_reduce_add_2d(&tmdq, stg, h * DH + rd * 64, row0 + i * BQ);
-          tma_reduce_add_2d(&tmdq, stg + ATOM, h * DH + rd * 64 + 32, row0 + i * BQ);
+          tma_reduce_add_2d(&tmdq, buf, h * DH + c * 32, row0 + i * BQ);
           bulk_commit();
         }
       }

@@ -1564,7 +1564,7 @@ __device__ __forceinline__ float bf_lo(uint32_t x) { return __uint_as_float(x <<
 __device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
 
 template <int DH>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three warps share SMSPs 0-2)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
                   const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse,
                   const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
@@ -1579,7 +1579,7 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *do_full = bar + 5, *do_empty = bar + 6,
            *s_full = bar + 7, *dp_full = bar + 8, *tdp_free = bar + 9, *p_ready = bar + 10, *ds_ready = bar + 11,
-           *mm2_done = bar + 12, *dq_done = bar + 13;
+           *mm2_done = bar + 12, *dq_done = bar + 13, *dv_done = bar + 15;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
   float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
   float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
@@ -1613,6 +1613,7 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(ds_ready, 128);
     mbar_init(mm2_done, 1);
     mbar_init(dq_done, 1);
+    mbar_init(dv_done, 1);
     fence_mbar_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -1644,30 +1645,31 @@ __global__ void __launch_bounds__(320, 1)
           tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, do_full, h * DH + a * 64, row0 + i * BQ);
       }
     }
-  } else if (warp == 9) {
-    {  // whole warp (converged: descriptors stay uniform), one elected lane issues
-      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
-      constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
-      constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
-      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS),
-                     sDO = smem_u32(sm + L::OFF_DO);
+  } else if (warp == 9 || warp == 10) {
+    // two MMA issuers on SMSPs 1 and 2, each a whole warp with one elected lane issuing:
+    //   warp 9  (X): dPᵀ_i (after dQ_{i−1} was drained), then Sᵀ_{i+1} (after dV_i has read Pᵀ_i)
+    //   warp 10 (Y): dV_i (after Pᵀ_i is written), then dQ_i, dK_i (after dSᵀ_i is in smem)
+    // an SMSP that issues MMAs loses issue slots to its other warps roughly while they execute: splitting the five
+    // products over two SMSPs halves what the compute warp sharing each one loses
+    constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
+    constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
+    constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
+    const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS),
+                   sDO = smem_u32(sm + L::OFF_DO);
+    if (warp == 9) {
       auto issue_s = [&](int it) {  // Sᵀ_it = K·Q_itᵀ into tS
         const int st = it & 1;
         mbar_wait(&q_full[st], (it >> 1) & 1);
         tc_fence_after();
         const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) {
-          umma_f16_w(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
-        }
+        for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
         umma_commit_w(s_full);
         TR(it, 0);
       };
       mbar_wait(kv_full, 0);
       issue_s(0);
       for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
         mbar_wait(do_full, it & 1);
         if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
         TR(it, 1);
@@ -1675,15 +1677,24 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
         umma_commit_w(dp_full);
+        if (it + 1 < n_it) {
+          mbar_wait(dv_done, it & 1);   // Sᵀ_{it+1} overwrites Pᵀ_it: only after dV_it has read it
+          issue_s(it + 1);
+        }
+      }
+    } else {
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1;
+        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
         mbar_wait(p_ready, it & 1);
+        mbar_wait(dp_full, it & 1);    // dPᵀ_it (issuer X) has read dO_i before dO is released below
         TR(it, 2);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA_w(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
         umma_commit_w(do_empty);
-        // Sᵀ_{it+1} right behind dV_it (same thread, in order: it overwrites Pᵀ_it only after dV_it has read it); the
-        // compute warps keep Pᵀ_it in registers for their dS pass, so Sᵀ_{it+1} is ready when that pass ends
-        if (it + 1 < n_it) issue_s(it + 1);
+        umma_commit_w(dv_done);
         mbar_wait(ds_ready, it & 1);
         TR(it, 3);
         // dQ_it precedes dK_it: its drain (which frees the TMEM columns dPᵀ_{it+1} needs) overlaps dK_it
@@ -2490,12 +2501,12 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   } else if (dh == 128) {
     static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<128><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
                                                                scale2, trace);
   } else {
     static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
     (void)once;
-    fa_bwd_kernel<64><<<grid, 320, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
+    fa_bwd_kernel<64><<<grid, 352, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
                                                              scale2, trace);
   }
   {

@@ -327,9 +327,12 @@ __global__ void __launch_bounds__(192, 1)
 //              warps 0-3 epilogue on own TMEM, releasing the accumulator on the leader's tempty (8 arrivals)
 //   leader:    warp 5 lane 0 issues the pair MMAs; tcgen05.commit multicasts smem-stage release (empty) and
 //              accumulator-ready (tfull) to both CTAs
+#ifndef GEMM2_STAGES
+#define GEMM2_STAGES 5   // 5 × 32 KB leaves room on the SM for a co-resident NCCL CTA at P > 1 (6 measured no faster at P = 1)
+#endif
 struct Gemm2Cfg {
   static constexpr int BN = 256;                      // pair tile N
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = GEMM2_STAGES;
   static constexpr int A_BYTES = BM * BK * 2;         // 16 KB: this CTA's 128 rows of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;

@@ -327,12 +327,10 @@ __global__ void __launch_bounds__(192, 1)
 //              warps 0-3 epilogue on own TMEM, releasing the accumulator on the leader's tempty (8 arrivals)
 //   leader:    warp 5 lane 0 issues the pair MMAs; tcgen05.commit multicasts smem-stage release (empty) and
 //              accumulator-ready (tfull) to both CTAs
-#ifndef GEMM2_STAGES
-#define GEMM2_STAGES 5   // 5 × 32 KB leaves room on the SM for a co-resident NCCL CTA at P > 1 (6 measured no faster at P = 1)
-#endif
+template <int NSTAGE>
 struct Gemm2Cfg {
   static constexpr int BN = 256;                      // pair tile N
-  static constexpr int STAGES = GEMM2_STAGES;
+  static constexpr int STAGES = NSTAGE;
   static constexpr int A_BYTES = BM * BK * 2;         // 16 KB: this CTA's 128 rows of A
   static constexpr int B_BYTES = (BN / 2) * BK * 2;   // 16 KB: this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -340,12 +338,12 @@ struct Gemm2Cfg {
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int NSTAGE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     void* __restrict__ C, int64_t ldc, const bf16* __restrict__ R, int M, int N, int K,
                     void* __restrict__ aux, int64_t ldx, int64_t I) {
-  using Cfg = Gemm2Cfg;
+  using Cfg = Gemm2Cfg<NSTAGE>;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -596,10 +594,10 @@ void dispatch_major(const GemmArgs& g, cudaStream_t s) {
 
 
 
-template <bool A_MN, bool B_MN, int EPI>
-void launch2(const GemmArgs& g, cudaStream_t s) {
-  using Cfg = Gemm2Cfg;
-  auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI>;
+template <bool A_MN, bool B_MN, int EPI, int NSTAGE>
+void launch2_n(const GemmArgs& g, cudaStream_t s) {
+  using Cfg = Gemm2Cfg<NSTAGE>;
+  auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI, NSTAGE>;
   static bool attr_set = false;
   static int max_clusters = 0;
   if (!attr_set) {
@@ -628,6 +626,21 @@ void launch2(const GemmArgs& g, cudaStream_t s) {
                                      static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
+}
+
+// shared-memory stages of the CTA-pair GEMM: 5 (default; leaves room on the SM for a co-resident NCCL CTA at P > 1)
+// or 6 (TAWPIPE_GEMM_STAGES=6).  Same box, C3: 5 stages +0.8 % at N = 1 and +1.1 % at N = 4 in the step, although a
+// cold, serialised ncu launch runs ≈10 % slower with 5 (less latency hidden from a cold L2)
+template <bool A_MN, bool B_MN, int EPI>
+void launch2(const GemmArgs& g, cudaStream_t s) {
+  static const int stages = [] {
+    const char* e = std::getenv("TAWPIPE_GEMM_STAGES");
+    return e ? std::atoi(e) : 5;
+  }();
+  if (stages == 5)
+    launch2_n<A_MN, B_MN, EPI, 5>(g, s);
+  else
+    launch2_n<A_MN, B_MN, EPI, 6>(g, s);
 }
 
 template <bool A_MN, bool B_MN>

@@ -147,9 +147,46 @@ def oracle_baseline(c, budget_s=20.0):
     fps = flops / dt
     tok_s = fps / flops_per_token(c)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    # a whole C0 step (BASELINE.json configs[0]) through the oracle as it stands, measured, not extrapolated
+    c0 = CONFIGS["c0"]
+    cfg0 = om.ModelConfig(n_layers=c0["L"], hidden=c0["H"], heads=c0["nh"], ffn=c0["I"], vocab=c0["V"], seq=c0["S"])
+    st0 = om.init_state(synth.init_params(c0["L"], c0["H"], c0["I"], c0["V"]))
+    toks0 = synth.tokens(4, 1, c0["S"], c0["V"])
+    t1 = time.perf_counter()
+    om.train_step(st0, toks0, cfg0)
+    c0_s = time.perf_counter() - t1
     return {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"one decoder layer (H={c['H']}, I={c['I']}) on S={S} tokens, fwd+recompute+bwd+AdamW "
-                      f"in {dt:.2f} s = {fps / 1e9:.1f} GFLOP/s fp64, extrapolated by FLOPs/token of the workload"}
+                      f"in {dt:.2f} s = {fps / 1e9:.1f} GFLOP/s fp64, extrapolated by FLOPs/token of the workload",
+            "c0_full_step": {"seconds": c0_s, "tokens_per_s": 4 * c0["S"] / c0_s,
+                             "what": "one whole C0 step (L=2, H=64, S=128, 4 micro-batches) of oracle.model.train_step"},
+            "host": host_info()}
+
+
+def host_info():
+    """CPU model and the BLAS numpy links (state the baseline's host)."""
+    info = {}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in ("Model name", "CPU(s)", "Thread(s) per core", "Socket(s)", "NUMA node(s)"):
+                info[k.strip()] = v.strip()
+    except Exception as e:
+        info["lscpu_error"] = str(e)[:80]
+    try:
+        import numpy as np
+        cfg = np.show_config(mode="dicts")
+        blas = cfg.get("Build Dependencies", {}).get("blas", {})
+        info["numpy_blas"] = f"{blas.get('name', '?')} {blas.get('version', '')}".strip()
+        try:
+            from threadpoolctl import threadpool_info
+            info["blas_threads"] = [p.get("num_threads") for p in threadpool_info() if p.get("user_api") == "blas"]
+        except Exception:
+            pass
+    except Exception as e:
+        info["blas_error"] = str(e)[:80]
+    return info
 
 
 def run_reference(args, c):
@@ -288,6 +325,8 @@ def run_ours(args, c):
             "exposed_ms": exposed, "overlapped_ms": max(0.0, st["weight_comm_ms"] + st["grad_comm_ms"] - exposed)}
     out = {
         "metric": METRIC, "value": tokens_step / (ms / 1e3), "unit": "tokens/s",
+        "value_is": f"whole-job tokens/s summed over all {world} GPU(s) (the bench contract); the metric's per-GPU "
+                    f"figure is tokens_per_s_per_gpu",
         "tokens_per_s_per_gpu": tokens_step / (ms / 1e3) / world,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if c["dtype"] else "f32",

@@ -187,9 +187,15 @@ const char* tawpipe_last_error(void);
 /* Free all device memory and communicators.  COLLECTIVE when world > 1. */
 void tawpipe_finalize(void);
 
-/* ---- kernel-level entry points (used by the per-op parity tests; device pointers) ---- */
+/* ---- kernel-level entry points ------------------------------------------------------------------------------
+ * Each runs exactly the kernel(s) tawpipe_step launches for that operation, on caller-owned DEVICE buffers of the
+ * caller's current device, asynchronously on `stream` (cudaStream_t; NULL = legacy default stream) unless stated.
+ * No context is needed.  Layouts are row-major; "dtype" is TAWPIPE_FP32 (fp32 tensors, SIMT kernels -- the fp32
+ * parity path) or TAWPIPE_BF16 (bf16 tensors, fp32 arithmetic inside, tcgen05 where the op is a contraction).
+ * Statistics (rstd, LSE, δ, loss rows) and accumulators are always fp32.  Return 0, TAWPIPE_ECONFIG (bad argument,
+ * message in tawpipe_last_error) or TAWPIPE_ERUNTIME (CUDA launch error).  They serve the per-op parity tests. */
 
-/* C[M,N] (+)= Σ_k A(m,k)·B(n,k) on `stream` (cudaStream_t, NULL = legacy default).
+/* C[M,N] (+)= Σ_k A(m,k)·B(n,k) (the QKV/O/MLP/head projections and their dgrad/wgrad).
  * A(m,k) = A[m·a_ld + k] if a_kmajor else A[k·a_ld + m]; likewise B(n,k).
  * dtype: TAWPIPE_BF16 (bf16 A/B, tcgen05, fp32 accumulate in TMEM) or TAWPIPE_FP32 (SIMT).
  * c_f32: C is fp32 (else the dtype); accumulate: C += result (else C = result);
@@ -201,18 +207,82 @@ int tawpipe_gemm(int dtype, int64_t M, int64_t N, int64_t K,
                  void* C, int64_t c_ld, int c_f32, int accumulate,
                  const void* R, void* stream);
 
-/* Causal attention forward on one micro-batch: qkv [B·S, 3H] (q | k | v column blocks,
- * head h at columns h·d_h of each block, RoPE already applied), o [B·S, H], lse fp32 [B][n_h][S]
- * (natural log).  dtype as above. */
+/* bf16 gate/up projection with the SwiGLU forward in the epilogue (the step's a5 MLP):
+ * [u | w] = x·W_guᵀ (x [M,K], W_gu [2I,K] = [W_gate ; W_up]); y [M,I] = SiLU(u)⊙w computed from the fp32
+ * accumulators; gu [M,2I] (nullable) receives [u | w] in bf16.  M, 2I mod 256 or 128, K mod 64 == 0. */
+int tawpipe_gemm_swiglu(int64_t M, int64_t I, int64_t K, const void* x, const void* w_gu, void* gu, void* y,
+                        void* stream);
+
+/* bf16 down-projection dgrad with the SwiGLU backward in the epilogue (the step's a7 MLP):
+ * dY = dh·W_down (dh [M,K], W_down [K,I]), then dgu [M,2I] = [dY⊙w⊙σ(u)(1+u(1−σ(u))) | dY⊙SiLU(u)] with
+ * u, w read from gu [M,2I] (SURVEY.md §8(c) SwiGLU backward); dY never reaches memory. */
+int tawpipe_gemm_swiglu_bwd(int64_t M, int64_t I, int64_t K, const void* dh, const void* w_down, const void* gu,
+                            void* dgu, void* stream);
+
+/* Causal attention forward on one micro-batch (SURVEY.md §8(c) step 2): qkv [B·S, 3H] (q | k | v column blocks,
+ * head h at columns h·d_h of each block, RoPE already applied), o [B·S, H], lse fp32 [B][n_h][S] (natural log).
+ * bf16 tcgen05 path: S mod 128 == 0, d_h ∈ {64, 128} (else a SIMT kernel). */
 int tawpipe_attention_fwd(int dtype, int B, int S, int n_h, int d_h,
                           const void* qkv, void* o, float* lse, void* stream);
 
 /* Causal attention backward: do_ [B·S, H] -> dqkv [B·S, 3H] (dq | dk | dv, w.r.t. the roped q,k).
- * `delta` is fp32 scratch of B·n_h·S floats; `dq_acc` fp32 scratch of B·S·H floats (may be NULL
- * for the fp32 path). */
+ * `scratch` is fp32 scratch of 2·B·n_h·S floats (δ = rowsum(dO⊙O) and the log2-domain LSE); `dq_acc` fp32
+ * scratch of B·S·H floats (may be NULL for the fp32 path). */
 int tawpipe_attention_bwd(int dtype, int B, int S, int n_h, int d_h,
                           const void* qkv, const void* o, const float* lse, const void* do_,
-                          void* dqkv, float* delta, float* dq_acc, void* stream);
+                          void* dqkv, float* scratch, float* dq_acc, void* stream);
+
+/* RMSNorm forward: y[r] = x[r]·rstd[r]⊙γ, rstd[r] = (mean_H(x[r]²) + eps)^(−1/2);
+ * x, y [rows, H] (dtype), γ [H] (dtype), rstd [rows] fp32. */
+int tawpipe_rmsnorm_fwd(int dtype, int64_t rows, int H, const void* x, const void* gamma, float eps, void* y,
+                        float* rstd, void* stream);
+
+/* RMSNorm backward: dx = (res ? res : 0) + rstd·(dy⊙γ) − x·rstd³·mean_H(dy⊙γ⊙x) written to dx [rows, H];
+ * dgamma_acc [H] fp32 += Σ_rows dy⊙x·rstd (accumulated, caller zeroes it).  res nullable (the residual stream
+ * gradient added in the same pass). */
+int tawpipe_rmsnorm_bwd(int dtype, int64_t rows, int H, const void* dy, const void* x, const void* gamma,
+                        const float* rstd, const void* res, void* dx, float* dgamma_acc, void* stream);
+
+/* Rotate-half RoPE in place on the q and k column blocks of qkv [B·S, 3·n_h·d_h]:
+ * x'_i = x_i cos − x_{i+d/2} sin, x'_{i+d/2} = x_{i+d/2} cos + x_i sin with angle p·theta^(−2i/d_h), p = row mod S;
+ * inverse != 0 rotates by −angle (the backward).  Tables are built in fp64 on the host, stored fp32, exactly as
+ * tawpipe_init builds them.  Synchronous (returns after the kernel completed). */
+int tawpipe_rope(int dtype, int B, int S, int n_h, int d_h, float theta, void* qkv, int inverse, void* stream);
+
+/* SwiGLU forward: gu [rows, 2I] = [u | w] -> y [rows, I] = SiLU(u)⊙w (the SIMT / fp32 path's separate kernel). */
+int tawpipe_swiglu_fwd(int dtype, int64_t rows, int I, const void* gu, void* y, void* stream);
+
+/* SwiGLU backward: dy [rows, I], gu [rows, 2I] -> dgu [rows, 2I] = [dy⊙w⊙σ(u)(1+u(1−σ(u))) | dy⊙SiLU(u)]. */
+int tawpipe_swiglu_bwd(int dtype, int64_t rows, int I, const void* dy, const void* gu, void* dgu, void* stream);
+
+/* Fused cross-entropy forward + backward: logits [rows, V] are overwritten in place with
+ * dz = (softmax(z) − onehot(target))·inv_denom; loss_rows [rows] fp32 = LSE(z) − z[target].  targets int32 [rows]
+ * in [0, V). */
+int tawpipe_cross_entropy(int dtype, int64_t rows, int V, void* logits, const int32_t* targets, float inv_denom,
+                          float* loss_rows, void* stream);
+
+/* Embedding forward: h[b·S + p] = E[tokens[b·tok_stride + p]], E [V, H], h [B·S, H]. */
+int tawpipe_embed_fwd(int dtype, int B, int S, const int32_t* tokens, int64_t tok_stride, const void* E, int H,
+                      void* h, void* stream);
+
+/* Deterministic embedding backward: dE [V, H] fp32 += Σ_{p : token_p = v} dh[p] with each token's positions
+ * summed in ascending order in fp32 (stable radix sort + segmented sum; bit-reproducible).  dh [B·S, H] (dtype).
+ * Allocates its sort scratch stream-ordered on `stream`. */
+int tawpipe_embed_bwd(int dtype, int B, int S, const int32_t* tokens, int64_t tok_stride, const void* dh, int H,
+                      int V, float* dE, void* stream);
+
+/* Fused gradient accumulation + AdamW on one owned stripe (a9; "updates ... applied at the owner";
+ * AdamW torch semantics, R1):
+ *   g = Σ_{groups gi ascending} ( Σ_{members, in order} srcs[·] )   in fp32 (R16),
+ *   θ ← θ(1 − lr·wd) unless no-decay; m ← β1 m + (1−β1) g; v ← β2 v + (1−β2) g²;
+ *   θ ← θ − lr·(m/(1−β1^step)) / (sqrt(v/(1−β2^step)) + eps);   wire ← wire_dtype(θ).
+ * group_sizes [n_groups] (1..8 groups, 1..16 sources in total); srcs [Σ sizes] device pointers of n elements, each
+ * fp32 if src_is_f32[i] else wire_dtype (any device memory the caller can address, including IPC-mapped peer
+ * memory); master / m / v fp32 [n] and wire [n] updated in place.  no_decay (nullable) = {lo0, hi0, lo1, hi1}: element
+ * i is not decayed if unit_off + i lies in [lo0, hi0) or [lo1, hi1).  hyper = {lr, β1, β2, eps, wd}; step >= 1. */
+int tawpipe_adamw(int wire_dtype, int n_groups, const int* group_sizes, const void* const* srcs, const int* src_is_f32,
+                  float* master, float* m, float* v, void* wire, int64_t n, int64_t unit_off,
+                  const int64_t* no_decay, const float* hyper, int step, void* stream);
 
 #ifdef __cplusplus
 }

@@ -171,6 +171,36 @@ def attention_row(i, q_i, k, v, do_i):
     return o_i, lse, dq_i
 
 
+def attention_fwd_rows(i0, i1, q, k, v):
+    """Query rows i0..i1−1 of attention_fwd for one head, with their LSE: the same definition evaluated for a
+    subset of rows (each row is independent), for spot checks at sizes where the S×S matrices do not fit.
+    q, k, v [S, d_h].  Returns (o [i1−i0, d_h], lse [i1−i0]) with lse_i = log Σ_{j ≤ i} exp(c·q_i·k_j)."""
+    dh = q.shape[1]
+    c = 1.0 / np.sqrt(dh)
+    s = c * (q[i0:i1] @ k[:i1].T)                              # [rows, i1]
+    s[np.arange(i1)[None, :] > np.arange(i0, i1)[:, None]] = -np.inf   # causal: key j > query i masked
+    mx = s.max(axis=1, keepdims=True)
+    e = np.exp(s - mx)
+    se = e.sum(axis=1, keepdims=True)
+    return (e / se) @ v[:i1], (mx + np.log(se))[:, 0]
+
+
+def attention_key_row(j, k_j, v_j, q, do, o, lse):
+    """Key row j of attention_bwd for one head: only query rows i ≥ j see key j (causal).
+    P_ij = exp(c·q_i·k_j − lse_i); dV_j = Σ_i P_ij do_i; dP_ij = do_i·v_j; δ_i = do_i·o_i; dS_ij = P_ij (dP_ij − δ_i);
+    dK_j = c Σ_i dS_ij q_i.  q, do, o [S, d_h] and lse [S] cover rows 0..S−1 (rows < j are not read)."""
+    dh = q.shape[1]
+    c = 1.0 / np.sqrt(dh)
+    qi, doi, oi = q[j:], do[j:], o[j:]
+    p = np.exp(c * (qi @ k_j) - lse[j:])
+    dv_j = p @ doi
+    dP = doi @ v_j
+    delta = np.sum(doi * oi, axis=1)
+    dS = p * (dP - delta)
+    dk_j = c * (dS @ qi)
+    return dk_j, dv_j
+
+
 def sigmoid(u):
     return 1.0 / (1.0 + np.exp(-u))
 

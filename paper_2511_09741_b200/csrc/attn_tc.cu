@@ -6,7 +6,7 @@
 //             P (bf16, smem) -> O += P·V (TMEM); O / l and LSE written at the end.
 //   backward: per 128-row key tile: Sᵀ = K·Qᵀ, dPᵀ = V·dOᵀ (TMEM) -> Pᵀ = exp(Sᵀ − LSE), dSᵀ = Pᵀ⊙(dPᵀ − δ)
 //             (bf16, smem) -> dV += Pᵀ·dO, dK += dSᵀ·Q (TMEM, persistent), dQ_i = dS·K (TMEM) reduced into an
-//             fp32 accumulator with vector atomics; δ = rowsum(dO⊙O) comes from a pre-pass.
+//             fp32 accumulator by TMA tensor reduce-add; δ = rowsum(dO⊙O) comes from a pre-pass.
 // Causal tiles above the diagonal are skipped (the masked half is work the method avoids, App. B).
 // Operand tiles are loaded once by TMA (128 rows × 64 columns, 128-byte swizzle); the same smem tile serves
 // as a K-major operand (Q, K for QKᵀ) and as an MN-major operand (V, dO, Q, K in the PV / gradient products).
@@ -14,7 +14,10 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <set>
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -47,7 +50,6 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 // element k of a 32-wide chunk: emulate 3 of every 8 exponentials on the FMA pipe
-__device__ __forceinline__ float ex2_mix(float x, int k) { return ex2(x); }  // emulation off: measured slower (r01)
 
 // packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2 / FMUL2: one issue slot for two lanes of work)
 __device__ __forceinline__ unsigned long long f2u(float2 a) {
@@ -106,450 +108,6 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t base, int ks) {
 }
 
 // =============================================================================================== forward
-template <int DH>
-struct FwdSmem {
-  static constexpr int QB = DH / 64 * ATOM;  // Q / K / V tile bytes
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = QB;           // 2 stages
-  static constexpr int OFF_V = 3 * QB;       // 2 stages
-  static constexpr int OFF_P = 5 * QB;       // 2 atoms
-  static constexpr int OFF_BAR = OFF_P + 2 * ATOM;
-  static constexpr int BYTES = OFF_BAR + 256 + 1024;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(192, 1)
-    fa_fwd_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
-                  int nh, float scale2) {
-  using L = FwdSmem<DH>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
-           *s_full = bar + 9, *p_full = bar + 11, *o_done = bar + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-
-  const int n_q = S / BQ;
-  // head-major order (the K/V of one head stay in L2 across its query tiles), heaviest tiles first in a head
-  const int qt = n_q - 1 - static_cast<int>(blockIdx.x % n_q);
-  const int h = static_cast<int>(blockIdx.x / n_q);
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int n_kv = qt + 1;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-    }
-    mbar_init(p_full, 128);
-    mbar_init(o_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, L::QB);
-      for (int a = 0; a < DH / 64; ++a)
-        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qt * BQ);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_expect_tx(&k_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_expect_tx(&v_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
-                      row0 + j * BQ);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q), sP = smem_u32(sm + L::OFF_P);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&k_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tS[st], desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
-        umma_commit(&k_empty[st]);
-        umma_commit(&s_full[st]);
-      };
-      mbar_wait(q_full, 0);
-      issue_s(0);
-      if (n_kv > 1) issue_s(1);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16(tO, desc_k(sP, ks), desc_mn(sV, ks), id_pv, (j | ks) > 0);
-        umma_commit(&v_empty[st]);
-        umma_commit(o_done);
-        if (j + 2 < n_kv) issue_s(j + 2);
-      }
-    }
-  } else {
-    // softmax warps: thread t <-> query row t of the tile (TMEM lane t)
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* sP = sm + L::OFF_P;
-    float m2 = -INFINITY, l = 0.f;
-    float s[128];
-    for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tS[st] + lane_off + c * 32, u);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]) * scale2;
-      }
-      if (j == qt) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (i > r) s[i] = -INFINITY;
-      }
-      float mx = s[0];
-#pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
-      if (j > 0) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} done: O stable, P buffer free
-      tc_fence_after();
-      if (j == 0) {
-        m2 = mx;
-      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
-        // lazy rescale (the stale max bounds P by 2^8); tcgen05.ld/st are warp-collective, so the whole warp
-        // rescales together, each row by its own factor (1 when its max did not grow)
-        const float mnew = fmaxf(m2, mx);
-        const float alpha = ex2(m2 - mnew);
-        l *= alpha;
-#pragma unroll 1
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld32(tO + lane_off + c * 32, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-          tmem_st32(tO + lane_off + c * 32, u);
-        }
-        tmem_wait_st();
-        m2 = mnew;
-      }
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        const float p = ex2_mix(s[i] - m2, i);
-        s[i] = p;
-        sum += p;
-      }
-      l += sum;
-      store_row_sw128(sP, r, s);
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(p_full);
-    }
-    mbar_wait(o_done, (n_kv - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t u[32];
-      tmem_ld32(tO + lane_off + c * 32, u);
-      tmem_wait_ld();
-      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o;
-        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
-        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
-        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
-        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
-        d4[v] = o;
-      }
-    }
-    lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ----------------------------------------------------------------------------------------------- forward v2
-// Two 128-row query tiles per CTA (A = tile 2t, B = tile 2t+1) with one softmax warpgroup each, so that the
-// exp work of one tile overlaps the tensor-core work of the other (ping-pong); P is written back into its
-// S columns of TMEM as packed bf16 and read from there as the A operand of O += P·V.
-//   warps 0-3: softmax A, warps 4-7: softmax B, warp 8: TMA producer, warp 9: MMA issuer (+ TMEM owner)
-//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
-template <int DH>
-struct Fwd2Smem {
-  static constexpr int QB = DH / 64 * ATOM;
-  static constexpr int OFF_Q = 0;        // Q_A, Q_B
-  static constexpr int OFF_K = 2 * QB;   // 2 stages
-  static constexpr int OFF_V = 4 * QB;   // 2 stages
-  static constexpr int OFF_BAR = 6 * QB;
-  static constexpr int BYTES = OFF_BAR + 256;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(320, 1)
-    fa_fwd2_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
-                   int nh, float scale2) {
-  using L = Fwd2Smem<DH>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
-           *s_full = bar + 9, *p_ready = bar + 11, *o_done = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-
-  const int n_q = S / BQ;
-  const int n_pair = (n_q + 1) / 2;
-  const int t = n_pair - 1 - static_cast<int>(blockIdx.x % n_pair);  // head-major, heaviest pairs first
-  const int h = static_cast<int>(blockIdx.x / n_pair);
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int qa = 2 * t, qb = 2 * t + 1;
-  const bool hasB = qb < n_q;
-  const int n_kv = hasB ? qb + 1 : qa + 1;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023) __trap();
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_ready[i], 128);
-      mbar_init(&o_done[i], 1);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 8) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, (hasB ? 2 : 1) * L::QB);
-      for (int a = 0; a < DH / 64; ++a) {
-        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qa * BQ);
-        if (hasB) tma_load_2d(sm + L::OFF_Q + L::QB + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qb * BQ);
-      }
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_expect_tx(&k_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_expect_tx(&v_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
-                      row0 + j * BQ);
-      }
-    }
-  } else if (warp == 9) {
-    if (lane == 0) {
-      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
-      const uint32_t sQ[2] = {smem_u32(sm + L::OFF_Q), smem_u32(sm + L::OFF_Q + L::QB)};
-      auto issue_s = [&](int w, int j) {
-        const uint32_t sK = smem_u32(sm + L::OFF_K + (j & 1) * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_f16(tmem + w * 128, desc_k(sQ[w], ks), desc_k(sK, ks), id_qk, ks > 0);
-        umma_commit(&s_full[w]);
-      };
-      auto issue_pv = [&](int w, int j) {
-        const uint32_t sV = smem_u32(sm + L::OFF_V + (j & 1) * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks)
-          umma_f16_tmemA(tmem + 256 + w * 128, tmem + w * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
-        umma_commit(&o_done[w]);
-      };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      if (hasB) issue_s(1, 0);
-      umma_commit(&k_empty[0]);
-      for (int j = 0; j < n_kv; ++j) {
-        const bool actA = j <= qa;
-        const bool next = j + 1 < n_kv;
-        if (next) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-        if (actA) {
-          mbar_wait(&p_ready[0], j & 1);
-          tc_fence_after();
-          issue_pv(0, j);
-          if (j + 1 <= qa) issue_s(0, j + 1);
-        }
-        if (hasB) {
-          mbar_wait(&p_ready[1], j & 1);
-          tc_fence_after();
-          issue_pv(1, j);
-          if (next) issue_s(1, j + 1);
-        }
-        umma_commit(&v_empty[j & 1]);
-        if (next) umma_commit(&k_empty[(j + 1) & 1]);
-      }
-    }
-  } else {
-    const int w = warp >> 2;        // 0: tile A, 1: tile B
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const int qt = w == 0 ? qa : qb;
-    if (w == 0 || hasB) {
-      const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-      const uint32_t tS = tmem + w * 128, tO = tmem + 256 + w * 128;
-      float m2 = -INFINITY, l = 0.f;
-      for (int j = 0; j <= qt; ++j) {
-        const bool diag = (j == qt);
-        mbar_wait(&s_full[w], j & 1);
-        tc_fence_after();
-        // pass 1: row max over the raw scores, two chunks per TMEM round trip, 8 independent chains
-        float mxa[8] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int cp = 0; cp < 4; cp += 2) {
-          uint32_t uu[2][32];
-          tmem_ld32(tS + lane_off + cp * 32, uu[0]);
-          tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
-          tmem_wait_ld();
-          if (diag) {
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-              for (int k = 0; k < 32; ++k)
-                if ((cp + h2) * 32 + k <= r) mxa[k & 7] = fmaxf(mxa[k & 7], __uint_as_float(uu[h2][k]));
-          } else {
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-              for (int k = 0; k < 32; ++k) mxa[k & 7] = fmaxf(mxa[k & 7], __uint_as_float(uu[h2][k]));
-          }
-        }
-        const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                               fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7]))) * scale2;
-        if (j == 0) {
-          m2 = mx;
-        } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
-          // lazy rescale of O (stable: PV_{j-1} completed before S_j was committed, in issue order)
-          const float mnew = fmaxf(m2, mx);
-          const float alpha = ex2(m2 - mnew);
-          l *= alpha;
-#pragma unroll 1
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t u[32];
-            tmem_ld32(tO + lane_off + c * 32, u);
-            tmem_wait_ld();
-#pragma unroll
-            for (int k = 0; k < 32; ++k) u[k] = __float_as_uint(__uint_as_float(u[k]) * alpha);
-            tmem_st32(tO + lane_off + c * 32, u);
-          }
-          m2 = mnew;
-        }
-        // pass 2: P = exp2(s·c·log2e − m), row sum (8 chains), packed bf16 back over the S columns
-        float sa[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int cp = 0; cp < 4; cp += 2) {
-          uint32_t uu[2][32];
-          tmem_ld32(tS + lane_off + cp * 32, uu[0]);
-          tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int c = cp + h2;
-            uint32_t pw[16];
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              float p0 = ex2_mix(fmaf(__uint_as_float(uu[h2][k]), scale2, -m2), k);
-              float p1 = ex2_mix(fmaf(__uint_as_float(uu[h2][k + 1]), scale2, -m2), k + 1);
-              if (diag) {
-                if (c * 32 + k > r) p0 = 0.f;
-                if (c * 32 + k + 1 > r) p1 = 0.f;
-              }
-              sa[k & 7] += p0;
-              sa[(k + 1) & 7] += p1;
-              pw[k / 2] = pack_bf16(p0, p1);
-            }
-            tmem_st16(tS + lane_off + c * 16, pw);  // P over S columns already read (c*16 < cp*32 + 64)
-          }
-        }
-        const float sum = ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
-        l += sum;
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_ready[w]);
-      }
-      mbar_wait(&o_done[w], qt & 1);
-      tc_fence_after();
-      const float inv = 1.f / l;
-      bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
-#pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tO + lane_off + c * 32, u);
-        tmem_wait_ld();
-        uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 o;
-          o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
-          o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
-          o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
-          o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
-          d4[v] = o;
-        }
-      }
-      lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
-      tc_fence_before();
-    }
-  }
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
 // ----------------------------------------------------------------------------------------------- forward v3
 // One 128-row query tile per CTA; S double-buffered in TMEM, P written back over its S columns (packed bf16)
 // and consumed from TMEM as the A operand of O += P·V.  The softmax of tile j therefore never waits for the
@@ -570,7 +128,7 @@ struct Fwd3Smem {
   static constexpr int BYTES = OFF_BAR + 256;
 };
 
-template <int DH, int EMU>
+template <int DH>
 __global__ void __launch_bounds__(224, 1)
     fa_fwd3_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
                    int nh, float scale2, unsigned long long* __restrict__ trace) {
@@ -753,8 +311,8 @@ __global__ void __launch_bounds__(224, 1)
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           const float2 a2 = ffma2(make_float2(s[c * 32 + i], s[c * 32 + i + 1]), sc2, nm2);
-          const float p0 = (EMU && ((i & 7) >= 8 - EMU)) ? ex2_poly(a2.x) : ex2(a2.x);
-          const float p1 = (EMU && (((i + 1) & 7) >= 8 - EMU)) ? ex2_poly(a2.y) : ex2(a2.y);
+          const float p0 = ex2(a2.x);
+          const float p1 = ex2(a2.y);
           sa2[(i >> 1) & 3] = fadd2(sa2[(i >> 1) & 3], make_float2(p0, p1));
           pw[i / 2] = pack_bf16(p0, p1);
         }
@@ -797,20 +355,6 @@ __global__ void __launch_bounds__(224, 1)
   }
 }
 
-// ----------------------------------------------------------------------------------------------- forward v5
-// Two query tiles per CTA (A = 2p+1, B = 2p: the same K/V stream, A one key tile longer) with one softmax
-// warpgroup each, so that one tile's exponentials run on the MUFU while the other tile's scores are loaded,
-// reduced and written back, and each tile's P·V / next S run on the tensor core under the other tile's softmax.  Each tile has one S/P buffer and one
-// O accumulator in TMEM (4 × 128 columns); S_t(j) is issued right behind P·V_t(j−1) by the same thread, so its
-// completion implies P·V_t(j−1)'s: O_t is stable whenever softmax t runs and the lazy rescale never waits.
-//   warps 0-3: softmax of tile A, warps 4-7: softmax of tile B (thread = row, lane quarter = warp % 4)
-//   warp 8: MMA issuer (P·V_t(j) then S_t(j+1), in order), warp 9: TMA producer (Q_A, Q_B once; K, V 2-stage rings)
-//   TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
-// Strict alternation of the two tiles' exponential passes (named-barrier ping-pong): measured 3-4 % slower than
-// letting both warpgroups run freely (two warps per SMSP keep the MUFU busier than one warp alternating), so off.
-#ifndef FWD5_PINGPONG
-#define FWD5_PINGPONG 0
-#endif
 template <int DH>
 struct Fwd5Smem {
   static constexpr int QB = DH / 64 * ATOM;
@@ -821,249 +365,10 @@ struct Fwd5Smem {
   static constexpr int OFF_BAR = 2 * QB + 2 * NST * QB;
   static constexpr int BYTES = OFF_BAR + 256;
 };
-
-// 320 threads; the bounds say 384 so that ptxas keeps to 168 registers (three warps share SMSPs 0 and 1)
-template <int DH>
-__global__ void __launch_bounds__(384, 1)
-    fa_fwd5_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
-                   int nh, float scale2, unsigned long long* __restrict__ trace) {
-  auto TR = [&](int it, int ev) {
-    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32) trace[it * 16 + ev] = clock64();
-  };
-  using L = Fwd5Smem<DH>;
-  constexpr int NST = L::NST;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
-           *v_empty = bar + 1 + 3 * NST, *s_full = bar + 1 + 4 * NST, *p_ready = bar + 3 + 4 * NST,
-           *pv_done = bar + 5 + 4 * NST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 7 + 4 * NST);
-
-  const int n_pairs = S / BQ / 2;
-  // head-major (K/V of a head stay in L2), heaviest pairs first within a head
-  const int pr = n_pairs - 1 - static_cast<int>(blockIdx.x % n_pairs);
-  const int h = static_cast<int>(blockIdx.x / n_pairs);
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int n_kv_A = 2 * pr + 2;   // tile B (2p) stops one key tile earlier
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023) __trap();
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&p_ready[t], 128);
-      mbar_init(&pv_done[t], 1);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 8) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 9) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, 2 * L::QB);
-      for (int t = 0; t < 2; ++t)
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_Q + t * L::QB + a * ATOM, &tm, q_full, h * DH + a * 64,
-                      row0 + (2 * pr + 1 - t) * BQ);
-      for (int j = 0; j < n_kv_A; ++j) {
-        const int st = j % NST;
-        const uint32_t ph = (j / NST) & 1;
-        mbar_wait_sleep(&k_empty[st], ph ^ 1);
-        mbar_expect_tx(&k_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
-        mbar_wait_sleep(&v_empty[st], ph ^ 1);
-        mbar_expect_tx(&v_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
-                      row0 + j * BQ);
-      }
-    }
-  } else if (warp == 8) {
-    // one issuer for both chains, in the order P·V_t(j), S_t(j+1) per tile: the tensor pipe executes one thread's
-    // MMAs in order, so S_t(j+1) overwrites tile t's P only after P·V_t(j) has read it, with no wait in between
-    constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
-    constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
-    auto issue_s = [&](int t, int jj) {
-      const uint32_t sK = smem_u32(sm + L::OFF_K + (jj % NST) * L::QB);
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q + t * L::QB);
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tmem + t * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
-      umma_commit_w(&s_full[t]);
-      TR(jj, 6 + t);
-    };
-    mbar_wait(q_full, 0);
-    mbar_wait(&k_full[0], 0);
-    tc_fence_after();
-    issue_s(0, 0);
-    issue_s(1, 0);
-    umma_commit_w(&k_empty[0]);
-    for (int j = 0; j < n_kv_A; ++j) {
-      const int st = j % NST;
-      mbar_wait(&v_full[st], (j / NST) & 1);
-      const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
-      const bool next = j + 1 < n_kv_A;
-      if (next) mbar_wait(&k_full[(j + 1) % NST], ((j + 1) / NST) & 1);
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (j >= n_kv_A - t) continue;   // tile B has one key tile fewer
-        mbar_wait(&p_ready[t], j & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks)
-          umma_f16_tmemA_w(tmem + 256 + t * 128, tmem + t * 128 + ks * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
-        umma_commit_w(&pv_done[t]);
-        TR(j, 8 + t);
-        if (j + 1 < n_kv_A - t) issue_s(t, j + 1);
-      }
-      umma_commit_w(&v_empty[st]);
-      if (next) umma_commit_w(&k_empty[(j + 1) % NST]);
-    }
-  } else {
-    const int t = warp >> 2;          // 0: tile A, 1: tile B
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const int qt = 2 * pr + 1 - t;
-    const int n_kv = qt + 1;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
-    float m2 = -INFINITY, l = 0.f;
-    float s[128];
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      if (r == 0) TR(j, 3 * t);
-      tc_fence_after();
-      {
-        uint32_t u0[32], u1[32], u2[32], u3[32];
-        tmem_ld32(tS, u0);
-        tmem_ld32(tS + 32, u1);
-        tmem_ld32(tS + 64, u2);
-        tmem_ld32(tS + 96, u3);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          s[i] = __uint_as_float(u0[i]);
-          s[32 + i] = __uint_as_float(u1[i]);
-          s[64 + i] = __uint_as_float(u2[i]);
-          s[96 + i] = __uint_as_float(u3[i]);
-        }
-      }
-      if (j == qt) {  // diagonal tile only
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (i > r) s[i] = -INFINITY;
-      }
-      float mxa[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mxa[k] = s[k];
-#pragma unroll
-      for (int i = 8; i < 128; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
-      float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-      mx *= scale2;
-      if (j == 0) {
-        m2 = mx;
-      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
-        // lazy rescale; O_t is stable here (S_t(j) was issued after P·V_t(j−1) completed)
-        const float mnew = fmaxf(m2, mx);
-        const float alpha = ex2(m2 - mnew);
-        l *= alpha;
-#pragma unroll 1
-        for (int c = 0; c < DH / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld32(tO + c * 32, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-          tmem_st32(tO + c * 32, u);
-        }
-        m2 = mnew;
-      }
-      // ping-pong: the two tiles take turns on the exponential pass (A_j, B_j, A_{j+1}, ...), so that one tile's
-      // loads / max / rescale / P store overlap the other tile's MUFU work (named barriers 1: A may go, 2: B may go)
-      if (FWD5_PINGPONG) {
-        if (t == 0) {
-          if (j > 0) named_bar(1, 256);
-        } else {
-          named_bar(2, 256);
-        }
-      }
-      if (r == 0) TR(j, 3 * t + 1);
-      float2 sa2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(-m2, -m2);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pw[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float2 a2 = ffma2(make_float2(s[c * 32 + i], s[c * 32 + i + 1]), sc2, nm2);
-          const float p0 = ex2(a2.x), p1 = ex2(a2.y);
-          sa2[(i >> 1) & 3] = fadd2(sa2[(i >> 1) & 3], make_float2(p0, p1));
-          pw[i / 2] = pack_bf16(p0, p1);
-        }
-        tmem_st16(tS + c * 16, pw);
-      }
-      if (r == 0) TR(j, 3 * t + 2);
-      if (FWD5_PINGPONG) {
-        if (t == 0) {
-          if (j < n_kv - 1) named_bar_arrive(2, 256);   // B's step j (tile B has n_kv − 1 steps)
-        } else {
-          named_bar_arrive(1, 256);                     // A's step j + 1
-        }
-      }
-      const float2 t2 = fadd2(fadd2(sa2[0], sa2[1]), fadd2(sa2[2], sa2[3]));
-      l += t2.x + t2.y;
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_ready[t]);
-    }
-    mbar_wait(&pv_done[t], (n_kv - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t u[32];
-      tmem_ld32(tO + c * 32, u);
-      tmem_wait_ld();
-      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o;
-        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
-        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
-        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
-        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
-        d4[v] = o;
-      }
-    }
-    lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 8) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
 // ----------------------------------------------------------------------------------------------- forward v7
-// As v5 (two query tiles per CTA, one softmax warpgroup each, one in-order MMA issuer), but every 128-key step is
+// Two query tiles per CTA (A = 2p+1, B = 2p: one K/V stream, A one key tile longer), one softmax warpgroup each
+// (thread = row), so one tile's exponentials run on the MUFU while the other tile's scores are loaded, reduced and
+// written back (the r01 "v5" design, superseded by this kernel and removed).  Every 128-key step is
 // processed as two 64-key halves with their own online-softmax update: S_t(j, half) is an N = 64 MMA, P_t(j, half)
 // goes back over the first 32 columns of its half, P·V_t(j, half) is a K = 64 MMA, and S_t(j+1, half) is issued
 // right behind it.  A tile's softmax therefore works on one half while the tensor core runs the other half's P·V
@@ -1291,246 +596,6 @@ __global__ void __launch_bounds__(384, 1)
   }
   __syncthreads();
   if (warp == 8) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ----------------------------------------------------------------------------------------------- forward v4
-// As v3, but the row softmax is split over two warps per SMSP: warp w (w = 2..9) handles rows 32(w%4).. and
-// key columns 64·h.. (h = half).  The two halves exchange their partial row maxima through smem once per
-// key tile (one named barrier); row sums stay per half until the end.  Each half writes its P columns into
-// its own S columns of TMEM and rescales its half of O.
-//   warps 0-7: softmax (half = w / 4, lane quarter = w % 4), warp 8: TMA producer, warp 9: MMA issuer
-//   TMEM: S0 [0,128) S1 [128,256) O [384,512) (two S/P buffers in flight, see NSB)
-template <int DH>
-struct Fwd4Smem {
-  static constexpr int QB = DH / 64 * ATOM;
-  static constexpr int NST = 3;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = QB;
-  static constexpr int OFF_V = QB + NST * QB;
-  static constexpr int OFF_RED = QB + 2 * NST * QB;   // [2 buffers][2 halves][128] partial maxima (then sums)
-  static constexpr int OFF_BAR = OFF_RED + 2 * 1024;
-  static constexpr int BYTES = OFF_BAR + 256;
-};
-
-template <int DH>
-__global__ void __launch_bounds__(320, 1)
-    fa_fwd4_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
-                   int nh, float scale2) {
-  using L = Fwd4Smem<DH>;
-  constexpr int NST = L::NST;
-  // S/P buffers in flight.  Must stay 2: the lazy rescale waits o_done by parity for P·V_{j-1}, which is
-  // only unambiguous while S_j being ready implies P·V_{j-2} has completed (S_j is issued after P·V_{j-NSB}).
-  // Three buffers measured no faster (r01) and break that invariant.
-  constexpr int NSB = 2;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
-           *v_empty = bar + 1 + 3 * NST, *s_full = bar + 1 + 4 * NST, *p_ready = bar + 4 + 4 * NST,
-           *o_done = bar + 7 + 4 * NST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 4 * NST);
-  float* red = reinterpret_cast<float*>(sm + L::OFF_RED);   // red[(buf * 2 + half) * 128 + row]
-
-  const int n_q = S / BQ;
-  // head-major order (the K/V of one head stay in L2 across its query tiles), heaviest tiles first in a head
-  const int qt = n_q - 1 - static_cast<int>(blockIdx.x % n_q);
-  const int h = static_cast<int>(blockIdx.x / n_q);
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int n_kv = qt + 1;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023) __trap();
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 3; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_ready[i], 256);
-    }
-    mbar_init(o_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 384;   // S/P buffers at 0, 128, 256
-
-  if (warp == 8) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, L::QB);
-      for (int a = 0; a < DH / 64; ++a)
-        tma_load_2d(sm + L::OFF_Q + a * ATOM, &tm, q_full, h * DH + a * 64, row0 + qt * BQ);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % NST;
-        const uint32_t ph = (j / NST) & 1;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_expect_tx(&k_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_K + st * L::QB + a * ATOM, &tm, &k_full[st], H + h * DH + a * 64, row0 + j * BQ);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_expect_tx(&v_full[st], L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_V + st * L::QB + a * ATOM, &tm, &v_full[st], 2 * H + h * DH + a * 64,
-                      row0 + j * BQ);
-      }
-    }
-  } else if (warp == 9) {
-    if (lane == 0) {
-      constexpr uint32_t id_qk = umma_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t id_pv = umma_idesc_bf16(128, DH, false, true);
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q);
-      auto issue_s = [&](int j) {
-        const int st = j % NST;
-        mbar_wait(&k_full[st], (j / NST) & 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(sm + L::OFF_K + st * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16(tmem + (j % NSB) * 128, desc_k(sQ, ks), desc_k(sK, ks), id_qk, ks > 0);
-        umma_commit(&k_empty[st]);
-        umma_commit(&s_full[j % NSB]);
-      };
-      mbar_wait(q_full, 0);
-      issue_s(0);
-      if (n_kv > 1) issue_s(1);
-      if (NSB > 2 && n_kv > 2) issue_s(2);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % NST;
-        mbar_wait(&p_ready[j % NSB], (j / NSB) & 1);
-        mbar_wait(&v_full[st], (j / NST) & 1);
-        tc_fence_after();
-        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::QB);
-        const uint32_t tP = tmem + (j % NSB) * 128;
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks)  // P: keys 0..63 at tP[0,32), keys 64..127 at tP[64,96)
-          umma_f16_tmemA(tO, tP + (ks >> 2) * 64 + (ks & 3) * 8, desc_mn(sV, ks), id_pv, (j | ks) > 0);
-        umma_commit(&v_empty[st]);
-        umma_commit(o_done);
-        if (j + NSB < n_kv) issue_s(j + NSB);   // overwrites S/P buffer (j % NSB) after P·V_j in issue order
-      }
-    }
-  } else {
-    const int hf = warp >> 2;           // key-column half
-    const int q = warp & 3;             // TMEM lane quarter
-    const int r = q * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    float m2 = -INFINITY, l = 0.f;
-    float s[64];
-    for (int j = 0; j < n_kv; ++j) {
-      const uint32_t tS = tmem + (j % NSB) * 128 + lane_off + hf * 64;
-      mbar_wait(&s_full[j % NSB], (j / NSB) & 1);
-      tc_fence_after();
-      {
-        uint32_t u0[32], u1[32];
-        tmem_ld32(tS, u0);
-        tmem_ld32(tS + 32, u1);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          s[i] = __uint_as_float(u0[i]);
-          s[32 + i] = __uint_as_float(u1[i]);
-        }
-      }
-      if (j == qt) {  // diagonal tile only
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (hf * 64 + i > r) s[i] = -INFINITY;
-      }
-      float mxa[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mxa[k] = s[k];
-#pragma unroll
-      for (int i = 8; i < 64; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
-      float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                       fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-      // combine the two halves' maxima (double-buffered by key tile parity)
-      float* rb = red + (j & 1) * 256;
-      rb[hf * 128 + r] = mx;
-      named_bar(1, 256);
-      mx = fmaxf(rb[r], rb[128 + r]) * scale2;
-      if (j == 0) {
-        m2 = mx;
-      } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
-        // rescale this half of O: needs P·V_{j-1} complete.  Both halves see the same combined maxima, so
-        // they take the same decision per row; the warp-uniform vote may differ between the two warps of a row,
-        // which only changes whether m2 is refreshed for rows whose max did not grow (alpha = 1 there).
-        mbar_wait(o_done, (j - 1) & 1);
-        tc_fence_after();
-        const float mnew = fmaxf(m2, mx);
-        const float alpha = ex2(m2 - mnew);
-        l *= alpha;
-#pragma unroll 1
-        for (int c = 0; c < DH / 64; ++c) {
-          uint32_t u[32];
-          const uint32_t ta = tO + lane_off + hf * (DH / 2) + c * 32;
-          tmem_ld32(ta, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-          tmem_st32(ta, u);
-        }
-        m2 = mnew;
-      }
-      float sa[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t pw[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2(fmaf(s[c * 32 + i], scale2, -m2));
-          const float p1 = ex2(fmaf(s[c * 32 + i + 1], scale2, -m2));
-          sa[i & 7] += p0;
-          sa[(i + 1) & 7] += p1;
-          pw[i / 2] = pack_bf16(p0, p1);
-        }
-        tmem_st16(tS + c * 16, pw);
-      }
-      l += ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7]));
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_ready[j % NSB]);
-    }
-    mbar_wait(o_done, (n_kv - 1) & 1);
-    tc_fence_after();
-    float* lsum = red + (n_kv & 1) * 256;   // the buffer not read in the last key tile
-    lsum[hf * 128 + r] = l;
-    named_bar(1, 256);
-    const float ltot = lsum[r] + lsum[128 + r];
-    const float inv = 1.f / ltot;
-    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH + hf * (DH / 2);
-#pragma unroll 1
-    for (int c = 0; c < DH / 64; ++c) {
-      uint32_t u[32];
-      tmem_ld32(tO + lane_off + hf * (DH / 2) + c * 32, u);
-      tmem_wait_ld();
-      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o;
-        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * inv, __uint_as_float(u[8 * v + 1]) * inv);
-        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * inv, __uint_as_float(u[8 * v + 3]) * inv);
-        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * inv, __uint_as_float(u[8 * v + 5]) * inv);
-        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * inv, __uint_as_float(u[8 * v + 7]) * inv);
-        d4[v] = o;
-      }
-    }
-    if (hf == 0) lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(ltot)) * (1.0f / LOG2E);
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -1875,363 +940,6 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
   }
 }
 
-template <int DH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
-    fa_bwd6_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
-                  const __grid_constant__ CUtensorMap tmdq, const __grid_constant__ CUtensorMap tmdq64,
-                  const float* __restrict__ lse,
-                  const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
-                  float scale, float scale2, unsigned long long* __restrict__ trace) {
-  using L = BwdSmem<DH>;
-  // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
-  auto TR = [&](int it, int ev) {
-    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32) trace[it * 16 + ev] = clock64();
-  };
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *do_full = bar + 5, *do_empty = bar + 6,
-           *s_full = bar + 7, *dp_full = bar + 8, *tdp_free = bar + 9, *p_ready = bar + 10, *ds_ready = bar + 11,
-           *mm2_done = bar + 12, *dq_done = bar + 13, *stg_full = bar + 16, *peer_free = bar + 17;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
-  float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
-  float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
-
-  const int n_q = S / BQ;
-  // CTA pairs (cluster of 2) on key tiles 2p and 2p+1 of one head, heaviest pairs first: rank r = key tile 2p + r
-  const uint32_t rank = cluster_ctarank();
-  const int cl = static_cast<int>(blockIdx.x >> 1);
-  const int jt = 2 * (cl % (n_q / 2)) + static_cast<int>(rank);
-  const int h = cl / (n_q / 2);
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int n_it = n_q - jt;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023) __trap();  // SW128 tiles need a 1024-byte aligned base
-    tma_prefetch(&tm);
-    tma_prefetch(&tmdo);
-    tma_prefetch(&tmdq);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-    }
-    mbar_init(do_full, 1);
-    mbar_init(do_empty, 1);
-    mbar_init(s_full, 1);
-    mbar_init(dp_full, 1);
-    mbar_init(tdp_free, 128);
-    mbar_init(p_ready, 128);
-    mbar_init(ds_ready, 128);
-    mbar_init(mm2_done, 1);
-    mbar_init(dq_done, 1);
-    mbar_init(stg_full, 64);   // the peer's 64 sender threads (one release.cluster arrive each)
-    mbar_init(peer_free, 1);   // the peer's reduce issuer: its staging buffer may be written
-    fence_mbar_init();
-  }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  cluster_sync();   // both CTAs' barriers initialised before any remote arrival
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
-
-  if (warp == 8) {
-    if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * L::QB);
-      for (int a = 0; a < DH / 64; ++a) {
-        tma_load_2d(sm + L::OFF_K + a * ATOM, &tm, kv_full, H + h * DH + a * 64, row0 + jt * BQ);
-        tma_load_2d(sm + L::OFF_V + a * ATOM, &tm, kv_full, 2 * H + h * DH + a * 64, row0 + jt * BQ);
-      }
-      for (int it = 0; it < n_it; ++it) {
-        const int i = jt + it, st = it & 1;
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], L::QB + 1024);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_Q + st * L::QB + a * ATOM, &tm, &q_full[st], h * DH + a * 64, row0 + i * BQ);
-        const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ;
-        bulk_load(lse_s + st * 128, lse + li, 512, &q_full[st]);
-        bulk_load(del_s + st * 128, delta + li, 512, &q_full[st]);
-        mbar_wait(do_empty, (it & 1) ^ 1);
-        mbar_expect_tx(do_full, L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, do_full, h * DH + a * 64, row0 + i * BQ);
-      }
-    }
-  } else if (warp == 9) {
-    {  // whole warp (converged: descriptors stay uniform), one elected lane issues
-      constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
-      constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
-      constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
-      const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS),
-                     sDO = smem_u32(sm + L::OFF_DO);
-      auto issue_s = [&](int it) {  // Sᵀ_it = K·Q_itᵀ into tS
-        const int st = it & 1;
-        mbar_wait(&q_full[st], (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) {
-          umma_f16_w(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
-        }
-        umma_commit_w(s_full);
-        TR(it, 0);
-      };
-      mbar_wait(kv_full, 0);
-      issue_s(0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
-        mbar_wait(do_full, it & 1);
-        if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
-        TR(it, 1);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
-        umma_commit_w(dp_full);
-        mbar_wait(p_ready, it & 1);
-        TR(it, 2);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_tmemA_w(tdV, tS + ks * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
-        umma_commit_w(do_empty);
-        // Sᵀ_{it+1} right behind dV_it (same thread, in order: it overwrites Pᵀ_it only after dV_it has read it); the
-        // compute warps keep Pᵀ_it in registers for their dS pass, so Sᵀ_{it+1} is ready when that pass ends
-        if (it + 1 < n_it) issue_s(it + 1);
-        mbar_wait(ds_ready, it & 1);
-        TR(it, 3);
-        // dQ_it precedes dK_it: its drain (which frees the TMEM columns dPᵀ_{it+1} needs) overlaps dK_it
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
-        umma_commit_w(dq_done);
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
-        umma_commit_w(&q_empty[st]);
-        umma_commit_w(mm2_done);
-      }
-    }
-  } else if (warp < 4) {
-    const int t = warp * 32 + lane;  // key row of the tile (TMEM lane)
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    uint8_t* sDS = sm + L::OFF_DS;
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
-      const float* ls = lse_s + st * 128;
-      const float* dl = del_s + st * 128;
-      mbar_wait(&q_full[st], (it >> 1) & 1);   // LSE_i, δ_i landed (bulk copies on the same barrier as Q_i)
-      mbar_wait(s_full, it & 1);
-      if (t == 0) TR(it, 4);
-      tc_fence_after();
-#pragma unroll
-      // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
-      uint32_t pk[4][16];   // Pᵀ_it, packed bf16, kept for the dS pass (Sᵀ_{it+1} overwrites its TMEM copy)
-      auto p_pass = [&](auto diag) {
-#pragma unroll
-        for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
-          uint32_t uu[2][32];
-          tmem_ld32(tS + lane_off + cp * 32, uu[0]);
-          tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int c = cp + h2;
-            uint32_t (&pw)[16] = pk[c];
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
-              const float2 a2 = ffma2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
-                                      make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
-              float p0 = ex2(a2.x);
-              float p1 = ex2(a2.y);
-              if (decltype(diag)::value) {  // query index < key index is masked
-                if (c * 32 + k < t) p0 = 0.f;
-                if (c * 32 + k + 1 < t) p1 = 0.f;
-              }
-              pw[k / 2] = pack_bf16(p0, p1);
-            }
-            tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < cp*32+64)
-          }
-        }
-      };
-      if (it == 0)
-        p_pass(std::true_type{});
-      else
-        p_pass(std::false_type{});
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_ready);
-      if (t == 0) TR(it, 5);
-      mbar_wait(dp_full, it & 1);
-      if (t == 0) TR(it, 6);
-      if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ of the previous tile consumed by dK / dQ
-      if (t == 0) TR(it, 7);
-      tc_fence_after();
-#pragma unroll
-      for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
-        uint32_t uu[2][32];
-        tmem_ld32(tdP + lane_off + cp * 32, uu[0]);
-        tmem_ld32(tdP + lane_off + cp * 32 + 32, uu[1]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int c = cp + h2;
-          const uint32_t (&pp)[16] = pk[c];
-          uint32_t d[16];
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            const float2 dl2 = *reinterpret_cast<const float2*>(dl + c * 32 + k);
-            const float2 ds2 = fmul2(make_float2(bf_lo(pp[k / 2]), bf_hi(pp[k / 2])),
-                                     fadd2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
-                                           make_float2(-dl2.x, -dl2.y)));
-            d[k / 2] = pack_bf16(ds2.x, ds2.y);
-          }
-          // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int chunk = (c & 1) * 4 + v;
-            *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
-                make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
-          }
-        }
-      }
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(ds_ready);
-      if (t == 0) TR(it, 8);
-      if (lane == 0) TR(it, 12 + warp);   // per-warp dS done
-    }
-    // dK (× softmax scale) and dV rows of this key tile
-    mbar_wait(mm2_done, (n_it - 1) & 1);
-    tc_fence_after();
-    bf16* dkp = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + H + h * DH;
-    bf16* dvp = dkp + H;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t u[32], w[32];
-      tmem_ld32(tdK + lane_off + c * 32, u);
-      tmem_ld32(tdV + lane_off + c * 32, w);
-      tmem_wait_ld();
-      uint4* k4 = reinterpret_cast<uint4*>(dkp + c * 32);
-      uint4* v4 = reinterpret_cast<uint4*>(dvp + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o, o2;
-        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * scale, __uint_as_float(u[8 * v + 1]) * scale);
-        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * scale, __uint_as_float(u[8 * v + 3]) * scale);
-        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * scale, __uint_as_float(u[8 * v + 5]) * scale);
-        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * scale, __uint_as_float(u[8 * v + 7]) * scale);
-        o2.x = pack_bf16(__uint_as_float(w[8 * v + 0]), __uint_as_float(w[8 * v + 1]));
-        o2.y = pack_bf16(__uint_as_float(w[8 * v + 2]), __uint_as_float(w[8 * v + 3]));
-        o2.z = pack_bf16(__uint_as_float(w[8 * v + 4]), __uint_as_float(w[8 * v + 5]));
-        o2.w = pack_bf16(__uint_as_float(w[8 * v + 6]), __uint_as_float(w[8 * v + 7]));
-        k4[v] = o;
-        v4[v] = o2;
-      }
-    }
-    tc_fence_before();
-  } else if (warp < 8) {
-    // dQ warps 4-7 (TMEM lane quarter warp % 4 = query rows 32q..32q+31 of dQ_i).  For the query tiles both CTAs of
-    // the pair visit (all but CTA 0's first), the two dQ_i partials are summed before the reduce-add into L2: CTA 0
-    // reduces rows 0-63, CTA 1 rows 64-127; the other half's owner receives the partner's rows into its staging
-    // buffer through distributed shared memory, adds its own and issues one 32 KB TMA reduce-add -- half the L2
-    // reduce traffic of unpaired CTAs.
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sm + L::OFF_STG;
-    const bool my_lo = q < 2;                          // this warp holds rows 0-63
-    const bool own = my_lo == (rank == 0);             // ... which this CTA reduces
-    const int r = t & 63;                              // row inside the half
-    const bool issuer = own && r == 0;                 // the thread that issues this CTA's half reduce
-    const uint32_t peer = rank ^ 1u;
-    int kk = 0;                                        // paired iterations so far
-    for (int it = 0; it < n_it; ++it) {
-      const int i = jt + it;
-      mbar_wait(dq_done, it & 1);    // dQ_i complete
-      tc_fence_after();
-      uint32_t u[DH / 32][32];
-#pragma unroll
-      for (int c = 0; c < DH / 32; ++c) tmem_ld32(tdP + lane_off + c * 32, u[c]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(tdp_free);                   // TMEM columns free for the next dPᵀ
-      if (rank == 0 && it == 0) {
-        // CTA 0's first query tile has no partner contribution: full 128-row reduce in two 64-column rounds
-#pragma unroll
-        for (int rd = 0; rd < DH / 64; ++rd) {
-          if (t == 0) bulk_wait_read0();
-          named_bar(2, 128);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              *reinterpret_cast<uint4*>(stg + hh * ATOM + t * 128 + ((jj ^ (t & 7)) << 4)) =
-                  make_uint4(u[rd * 2 + hh][4 * jj], u[rd * 2 + hh][4 * jj + 1], u[rd * 2 + hh][4 * jj + 2],
-                             u[rd * 2 + hh][4 * jj + 3]);
-          fence_async_smem();
-          named_bar(2, 128);
-          if (t == 0) {
-            tma_reduce_add_2d(&tmdq, stg, h * DH + rd * 64, row0 + i * BQ);
-            tma_reduce_add_2d(&tmdq, stg + ATOM, h * DH + rd * 64 + 32, row0 + i * BQ);
-            bulk_commit();
-          }
-        }
-        continue;
-      }
-      // paired query tile: staging layout = the half's 64 rows × DH fp32 as DH/32 boxes of (32 columns × 64 rows)
-      if (own) {
-        if (issuer) {                            // our staging buffer is read: the peer may write into it
-          bulk_wait_read0();
-          mbar_arrive_cluster(mapa_shared(peer_free, peer));
-        }
-        mbar_wait_cluster(stg_full, kk & 1);     // the peer's rows have landed
-#pragma unroll
-        for (int c = 0; c < DH / 32; ++c)
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            uint4* a = reinterpret_cast<uint4*>(stg + c * 8192 + r * 128 + ((jj ^ (r & 7)) << 4));
-            uint4 v = *a;
-            v.x = __float_as_uint(__uint_as_float(v.x) + __uint_as_float(u[c][4 * jj]));
-            v.y = __float_as_uint(__uint_as_float(v.y) + __uint_as_float(u[c][4 * jj + 1]));
-            v.z = __float_as_uint(__uint_as_float(v.z) + __uint_as_float(u[c][4 * jj + 2]));
-            v.w = __float_as_uint(__uint_as_float(v.w) + __uint_as_float(u[c][4 * jj + 3]));
-            *a = v;
-          }
-        fence_async_smem();
-        named_bar(3, 64);
-        if (issuer) {
-#pragma unroll
-          for (int c = 0; c < DH / 32; ++c)
-            tma_reduce_add_2d(&tmdq64, stg + c * 8192, h * DH + c * 32, row0 + i * BQ + (rank == 0 ? 0 : 64));
-          bulk_commit();
-        }
-      } else {
-        mbar_wait(peer_free, kk & 1);            // the peer's staging buffer may be written
-        const uint32_t base = mapa_shared(stg, peer);
-#pragma unroll
-        for (int c = 0; c < DH / 32; ++c)
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            st_cluster_v4(base + c * 8192 + r * 128 + ((jj ^ (r & 7)) << 4), u[c][4 * jj], u[c][4 * jj + 1],
-                          u[c][4 * jj + 2], u[c][4 * jj + 3]);
-        mbar_arrive_cluster(mapa_shared(stg_full, peer));
-      }
-      ++kk;
-    }
-    if (t == 0 || issuer) bulk_wait_all0();
-  }
-  tc_fence_before();
-  cluster_sync();   // the peer's remote arrivals and staging writes are done before either CTA exits
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
 
 // δ_i = Σ_d dO_id·O_id ; one warp per (row, head)
 __global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16* __restrict__ o,
@@ -2304,167 +1012,93 @@ __global__ void fa_dq_convert_kernel(int64_t rows, int H, const float* __restric
   }
 }
 
+// Raise the dynamic shared-memory limit of `kern` once per (kernel, device): the attribute is per device, and a
+// process may bootstrap onto another GPU after a finalize.
 template <typename K>
 void prep(K kern, int bytes) {
-  TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  TP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert({reinterpret_cast<const void*>(kern), dev}).second)
+    TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
+
+// TAWPIPE_FA_TRACE=1: per-call clock64 timeline of CTA 0's first 32 key tiles (a tuning aid; allocated and freed
+// per call, never on the default path)
+struct FaTrace {
+  unsigned long long* p = nullptr;
+  FaTrace() {
+    if (std::getenv("TAWPIPE_FA_TRACE")) {
+      TP_CUDA(cudaMalloc(&p, 32 * 16 * 8));
+      TP_CUDA(cudaMemset(p, 0, 32 * 16 * 8));
+    }
+  }
+  void dump(const char* const* names, int t0_ev) {
+    if (!p) return;
+    unsigned long long h[32 * 16];
+    TP_CUDA(cudaMemcpy(h, p, sizeof(h), cudaMemcpyDeviceToHost));
+    const unsigned long long t0 = h[t0_ev];
+    for (int it = 0; it < 12; ++it) {
+      std::fprintf(stderr, "it %2d:", it);
+      for (int e = 0; e < 16 && names[e]; ++e) std::fprintf(stderr, " %s=%lld", names[e], (long long)(h[it * 16 + e] - t0));
+      std::fprintf(stderr, "\n");
+    }
+  }
+  ~FaTrace() {
+    if (p) cudaFree(p);
+  }
+};
 
 }  // namespace
 
 bool attention_tc_supported(int S, int dh) { return S % 128 == 0 && (dh == 64 || dh == 128); }
 
+// Forward: fa_fwd7 (two query tiles per CTA) when the number of query tiles is even, else fa_fwd3.
 void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, float* lse, cudaStream_t s) {
   TP_CHECK(attention_tc_supported(S, dh), TAWPIPE_ECONFIG, "tcgen05 attention: S % 128 == 0, d_h in {64, 128}");
   const int H = nh * dh;
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, static_cast<int64_t>(B) * S, 3ll * H, 128);
   const float scale2 = LOG2E / sqrtf(static_cast<float>(dh));
-  static const int fwd_env = [] {
-    const char* e = std::getenv("TAWPIPE_FA_FWD");
-    return e ? std::atoi(e) : 7;
-  }();
-  static unsigned long long* ftrace = [] {
-    unsigned long long* p = nullptr;
-    if (std::getenv("TAWPIPE_FA_TRACE")) {
-      cudaMalloc(&p, 32 * 16 * 8);
-      cudaMemset(p, 0, 32 * 16 * 8);
-    }
-    return p;
-  }();
-  // v5 pairs query tiles: needs an even number of them (else v3)
-  const int fwd_ver = ((fwd_env == 5 || fwd_env == 7) && (S / BQ) % 2 != 0) ? 3 : fwd_env;
-  if (fwd_ver == 7) {
+  if ((S / BQ) % 2 == 0) {
     dim3 grid7(static_cast<unsigned>((S / BQ / 2) * nh), static_cast<unsigned>(B));
     if (dh == 128) {
-      static bool once = (prep(fa_fwd7_kernel<128>, Fwd5Smem<128>::BYTES), true);
-      (void)once;
+      prep(fa_fwd7_kernel<128>, Fwd5Smem<128>::BYTES);
       fa_fwd7_kernel<128><<<grid7, 352, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
     } else {
-      static bool once = (prep(fa_fwd7_kernel<64>, Fwd5Smem<64>::BYTES), true);
-      (void)once;
+      prep(fa_fwd7_kernel<64>, Fwd5Smem<64>::BYTES);
       fa_fwd7_kernel<64><<<grid7, 352, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
     }
-    TP_CUDA(cudaGetLastError());
-    g_kstats.launches++;
-    return;
-  }
-  if (fwd_ver == 5) {
-    dim3 grid5(static_cast<unsigned>((S / BQ / 2) * nh), static_cast<unsigned>(B));
-    if (dh == 128) {
-      static bool once = (prep(fa_fwd5_kernel<128>, Fwd5Smem<128>::BYTES), true);
-      (void)once;
-      fa_fwd5_kernel<128><<<grid5, 320, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);
-    } else {
-      static bool once = (prep(fa_fwd5_kernel<64>, Fwd5Smem<64>::BYTES), true);
-      (void)once;
-      fa_fwd5_kernel<64><<<grid5, 320, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);
-    }
-    TP_CUDA(cudaGetLastError());
-    g_kstats.launches++;
-    if (ftrace) {
-      unsigned long long hb[32 * 16];
-      TP_CUDA(cudaMemcpy(hb, ftrace, sizeof(hb), cudaMemcpyDeviceToHost));
-      const unsigned long long t0 = hb[0];
-      auto T = [&](int it, int e) { return (long long)(hb[it * 16 + e] - t0); };
-      for (int it = 0; it < 12; ++it)
-        std::fprintf(stderr, "fwd5 j %2d: A s_full=%lld exp=%lld..%lld | B s_full=%lld exp=%lld..%lld | S_A=%lld S_B=%lld PV_A=%lld PV_B=%lld\n",
-                     it, T(it, 0), T(it, 1), T(it, 2), T(it, 3), T(it, 4), T(it, 5), T(it, 6), T(it, 7), T(it, 8), T(it, 9));
-    }
-    return;
-  }
-  if (fwd_ver == 4) {
-    dim3 grid4(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
-    if (dh == 128) {
-      static bool once = (prep(fa_fwd4_kernel<128>, Fwd4Smem<128>::BYTES), true);
-      (void)once;
-      fa_fwd4_kernel<128><<<grid4, 320, Fwd4Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
-    } else {
-      static bool once = (prep(fa_fwd4_kernel<64>, Fwd4Smem<64>::BYTES), true);
-      (void)once;
-      fa_fwd4_kernel<64><<<grid4, 320, Fwd4Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
-    }
-    TP_CUDA(cudaGetLastError());
-    g_kstats.launches++;
-    return;
-  }
-
-  if (fwd_ver == 3) {
-    static const int emu = [] {
-      const char* e = std::getenv("TAWPIPE_FA_EMU");   // exponentials per 8 computed on the FMA pipe
-      return e ? std::atoi(e) : 0;
-    }();
-    dim3 grid3(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
-#define FWD3_LAUNCH(D, E)                                                                              \
-  do {                                                                                                 \
-    static bool once = (prep(fa_fwd3_kernel<D, E>, Fwd3Smem<D>::BYTES), true);                        \
-    (void)once;                                                                                        \
-    fa_fwd3_kernel<D, E><<<grid3, 224, Fwd3Smem<D>::BYTES, s>>>(tm, o, lse, S, nh, scale2, ftrace);   \
-  } while (0)
-    if (dh == 128) {
-      if (emu == 1) FWD3_LAUNCH(128, 1);
-      else if (emu == 2) FWD3_LAUNCH(128, 2);
-      else if (emu == 3) FWD3_LAUNCH(128, 3);
-      else if (emu == 4) FWD3_LAUNCH(128, 4);
-      else FWD3_LAUNCH(128, 0);
-    } else {
-      FWD3_LAUNCH(64, 0);
-    }
-#undef FWD3_LAUNCH
-    TP_CUDA(cudaGetLastError());
-    g_kstats.launches++;
-    if (ftrace) {
-      unsigned long long hbuf[32 * 16];
-      TP_CUDA(cudaMemcpy(hbuf, ftrace, sizeof(hbuf), cudaMemcpyDeviceToHost));
-      const unsigned long long t0 = hbuf[3];
-      for (int it = 0; it < 12; ++it)
-        std::fprintf(stderr, "fwd j %2d: mma:p_ready=%lld mma:v_full=%lld mma:issued=%lld smx:s_full=%lld smx:p_done w0..3=%lld %lld %lld %lld\n", it,
-                     (long long)(hbuf[it * 16] - t0), (long long)(hbuf[it * 16 + 1] - t0), (long long)(hbuf[it * 16 + 2] - t0),
-                     (long long)(hbuf[it * 16 + 3] - t0), (long long)(hbuf[it * 16 + 4] - t0), (long long)(hbuf[it * 16 + 5] - t0),
-                     (long long)(hbuf[it * 16 + 6] - t0), (long long)(hbuf[it * 16 + 7] - t0));
-    }
-    return;
-  }
-  if (fwd_ver == 2) {
-    dim3 grid2(static_cast<unsigned>(((S / BQ + 1) / 2) * nh), static_cast<unsigned>(B));
-    if (dh == 128) {
-      static bool once = (prep(fa_fwd2_kernel<128>, Fwd2Smem<128>::BYTES), true);
-      (void)once;
-      fa_fwd2_kernel<128><<<grid2, 320, Fwd2Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
-    } else {
-      static bool once = (prep(fa_fwd2_kernel<64>, Fwd2Smem<64>::BYTES), true);
-      (void)once;
-      fa_fwd2_kernel<64><<<grid2, 320, Fwd2Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
-    }
-    TP_CUDA(cudaGetLastError());
-    g_kstats.launches++;
-    return;
-  }
-  dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
-  if (dh == 128) {
-    static bool once = (prep(fa_fwd_kernel<128>, FwdSmem<128>::BYTES), true);
-    (void)once;
-    fa_fwd_kernel<128><<<grid, 192, FwdSmem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
   } else {
-    static bool once = (prep(fa_fwd_kernel<64>, FwdSmem<64>::BYTES), true);
-    (void)once;
-    fa_fwd_kernel<64><<<grid, 192, FwdSmem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    FaTrace tr;
+    dim3 grid3(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
+    if (dh == 128) {
+      prep(fa_fwd3_kernel<128>, Fwd3Smem<128>::BYTES);
+      fa_fwd3_kernel<128><<<grid3, 224, Fwd3Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2, tr.p);
+    } else {
+      prep(fa_fwd3_kernel<64>, Fwd3Smem<64>::BYTES);
+      fa_fwd3_kernel<64><<<grid3, 224, Fwd3Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2, tr.p);
+    }
+    TP_CUDA(cudaGetLastError());
+    static const char* names[16] = {"mma:p_ready", "mma:v_full", "mma:issued", "smx:s_full", "smx:p_done", nullptr};
+    tr.dump(names, 3);
   }
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }
 
+// Backward: δ / log2-domain LSE pre-pass, fa_bwd (dK, dV in TMEM; dQ reduce-added into the fp32 dq_acc), then the
+// scaled dQ conversion into dqkv.  scratch: 2·B·n_h·S floats (δ, then LSE·log2e), owned by the caller.
 void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16* o, const float* lse,
-                      const bf16* dout, bf16* dqkv, float* delta, float* dq_acc, cudaStream_t s) {
+                      const bf16* dout, bf16* dqkv, float* scratch, float* dq_acc, cudaStream_t s) {
   TP_CHECK(attention_tc_supported(S, dh), TAWPIPE_ECONFIG, "tcgen05 attention: S % 128 == 0, d_h in {64, 128}");
-  TP_CHECK(dq_acc != nullptr, TAWPIPE_ECONFIG, "tcgen05 attention backward needs the fp32 dq accumulator");
+  TP_CHECK(dq_acc != nullptr && scratch != nullptr, TAWPIPE_ECONFIG,
+           "tcgen05 attention backward needs the δ/LSE scratch and the fp32 dq accumulator");
   const int H = nh * dh;
   const int64_t rows = static_cast<int64_t>(B) * S;
-  static float* lse2 = nullptr;
-  static int64_t lse2_n = 0;
-  if (lse2_n < rows * nh) {
-    if (lse2) TP_CUDA(cudaFree(lse2));
-    TP_CUDA(cudaMalloc(&lse2, rows * nh * sizeof(float)));
-    lse2_n = rows * nh;
-  }
+  float* delta = scratch;
+  float* lse2 = scratch + rows * nh;
   if (H % 32 == 0 && H / 32 <= 1024 && (dh == 64 || dh == 128))
     fa_delta_v8_kernel<<<static_cast<unsigned>(rows), H / 32, 0, s>>>(S, nh, dh, o, dout, delta, lse, lse2);
   else
@@ -2477,66 +1111,23 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   const float scale = 1.0f / sqrtf(static_cast<float>(dh));
   const float scale2 = LOG2E * scale;
   dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
-  static unsigned long long* trace = [] {
-    unsigned long long* p = nullptr;
-    if (std::getenv("TAWPIPE_FA_TRACE")) {
-      cudaMalloc(&p, 32 * 16 * 8);
-      cudaMemset(p, 0, 32 * 16 * 8);
-    }
-    return p;
-  }();
-  static const int bwd_ver = [] {
-    const char* e = std::getenv("TAWPIPE_FA_BWD");
-    return e ? std::atoi(e) : 5;
-  }();
-  if (dh == 128 && bwd_ver == 6 && (S / BQ) % 2 == 0) {
-    // v6 (experimental, off by default): CTA pairs summing their dQ partials through distributed shared memory
-    // (half the L2 reduce traffic).  Correct, but measured 2× slower at C3: with one staging buffer per CTA the
-    // per-tile exchange couples the two CTAs' pipelines so that they alternate instead of overlapping.
-    CUtensorMap tmdq64 = make_tmap_f32_2d(dq_acc, H, rows, H, 64);
-    static bool once = (prep(fa_bwd6_kernel<128>, BwdSmem<128>::BYTES), true);
-    (void)once;
-    fa_bwd6_kernel<128><<<grid, 320, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, tmdq64, lse2, delta, dq_acc, dqkv, S,
-                                                                nh, scale, scale2, trace);
-  } else if (dh == 128) {
-    static bool once = (prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES), true);
-    (void)once;
+  FaTrace tr;
+  if (dh == 128) {
+    prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES);
     fa_bwd_kernel<128><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                               scale2, trace);
+                                                               scale2, tr.p);
   } else {
-    static bool once = (prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES), true);
-    (void)once;
+    prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES);
     fa_bwd_kernel<64><<<grid, 352, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                             scale2, trace);
-  }
-  {
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-      cudaFuncAttributes a{};
-      if (dh == 128) cudaFuncGetAttributes(&a, fa_bwd_kernel<128>);
-      else cudaFuncGetAttributes(&a, fa_bwd_kernel<64>);
-      throw Error(TAWPIPE_ERUNTIME, std::string("fa_bwd launch: ") + cudaGetErrorString(e) + " regs " +
-                                        std::to_string(a.numRegs) + " maxThreads " + std::to_string(a.maxThreadsPerBlock) +
-                                        " static smem " + std::to_string(a.sharedSizeBytes) + " max dyn " +
-                                        std::to_string(a.maxDynamicSharedSizeBytes) + " requested dyn " +
-                                        std::to_string(dh == 128 ? BwdSmem<128>::BYTES : BwdSmem<64>::BYTES));
-    }
-  }
-  fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
-  if (trace) {
-    unsigned long long h[32 * 16];
-    TP_CUDA(cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost));
-    static const char* names[16] = {"mma:S_issued", "mma:dO+tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
-                                    "cmp:p_done", "cmp:dp_full", "cmp:mm2_prev", "cmp:ds_done", "dq:mm2_done",
-                                    "dq:tdp_free", "dq:staged", "cmp:ds_w0", "cmp:ds_w1", "cmp:ds_w2", "cmp:ds_w3"};
-    const unsigned long long t0 = h[0];
-    for (int it = 0; it < 12; ++it) {
-      std::fprintf(stderr, "it %2d:", it);
-      for (int e = 0; e < 16; ++e) std::fprintf(stderr, " %s=%lld", names[e], (long long)(h[it * 16 + e] - t0));
-      std::fprintf(stderr, "\n");
-    }
+                                                             scale2, tr.p);
   }
   TP_CUDA(cudaGetLastError());
+  fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
+  TP_CUDA(cudaGetLastError());
+  static const char* names[16] = {"mma:S_issued", "mma:dO+tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
+                                  "cmp:p_done", "cmp:dp_full", "cmp:mm2_prev", "cmp:ds_done", "dq:mm2_done",
+                                  "dq:tdp_free", "dq:staged", "cmp:ds_w0", "cmp:ds_w1", "cmp:ds_w2", "cmp:ds_w3"};
+  tr.dump(names, 0);
   g_kstats.launches += 3;
 }
 

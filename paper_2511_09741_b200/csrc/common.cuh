@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "tawpipe.h"
 
@@ -80,15 +81,20 @@ template <typename T>
 void attention_bwd_simt(int B, int S, int nh, int dh, const T* qkv, const T* o, const float* lse, const T* dout,
                         T* dqkv, float* delta, cudaStream_t s);
 void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, float* lse, cudaStream_t s);
+// scratch: 2·B·n_h·S floats (δ and the log2-domain LSE); dq_acc: B·S·H floats
 void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16* o, const float* lse,
-                      const bf16* dout, bf16* dqkv, float* delta, float* dq_acc, cudaStream_t s);
+                      const bf16* dout, bf16* dqkv, float* scratch, float* dq_acc, cudaStream_t s);
 bool attention_tc_supported(int S, int dh);
 
 // ---------------------------------------------------------------- elementwise / norm / loss / optimizer
 template <typename T>
 void embed_fwd(const int32_t* tok, int64_t tok_stride_seq, int B, int S, const T* E, int H, T* h, cudaStream_t s);
-void embed_bwd(const int32_t* tok, int64_t tok_stride_seq, int B, int S, const void* dh, bool dh_f32, int H,
-               float* dE, cudaStream_t s);
+// Deterministic embedding backward (embed.cu): dE[v] += Σ_{p : tok[p] = v} dh[p], the positions of each token summed
+// in ascending order in fp32 (a stable radix sort of (token, position) pairs, then one segment per token), so the
+// result is bit-reproducible run to run.  scratch: embed_bwd_scratch_bytes(B·S) bytes, device.
+size_t embed_bwd_scratch_bytes(int64_t T);
+void embed_bwd(const int32_t* tok, int64_t tok_stride_seq, int B, int S, const void* dh, bool dh_f32, int H, int V,
+               float* dE, void* scratch, size_t scratch_bytes, cudaStream_t s);
 template <typename T>
 void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s);
 // dx = (res ? res : 0) + RMSNorm'(dy); dg_acc += Σ_rows dy⊙x⊙r (fp32)
@@ -124,11 +130,39 @@ struct AdamParams {
   float lr, beta1, beta2, eps, wd;
   float bc1, bc2;  // 1 - beta^t
 };
-// Sum the D group contributions (ascending k; contribution own_k may be fp32) and apply AdamW
-// to the owned stripe [off, off+n) of a unit whose no-decay ranges are nd[0..n_nd).
+struct AdamRanges {  // no-decay ranges [lo, hi) in unit coordinates (RMSNorm gains, R1); empty ranges: lo = hi = 0
+  int64_t lo[2] = {0, 0}, hi[2] = {0, 0};
+};
+// Gradient sources of one owned stripe, grouped: group gi holds sources [group_end[gi−1], group_end[gi]) (member
+// order); bit si of f32_mask: source si is fp32, else the wire dtype.  Pointers may be peer (IPC-mapped) memory.
+struct GradSources {
+  const void* p[16] = {};
+  int n_groups = 0;
+  int group_end[8] = {};
+  unsigned f32_mask = 0;
+};
+// g = Σ_groups Σ_members (fp32), then AdamW on master / m / v [n] and wire[n] = W(master) (a9)
 template <typename W>
-void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_f32, float* master, float* m,
-                 float* v, W* wire, int64_t n, int64_t unit_off, const int64_t* nd_lo, const int64_t* nd_hi,
-                 int n_nd, AdamParams p, cudaStream_t s);
+void adamw_grouped(const GradSources& src, float* master, float* m, float* v, W* wire, int64_t n, int64_t unit_off,
+                   const AdamRanges& nd, const AdamParams& p, cudaStream_t s);
+
+// cos / sin of p·θ_i, θ_i = theta^(−2i/d_h), i < d_h/2, p < S: computed in fp64, stored fp32 (R10, R13); [S][d_h/2]
+void rope_tables_host(int S, int dh, double theta, std::vector<float>& cos_t, std::vector<float>& sin_t);
+
+// ---------------------------------------------------------------- errors at the C ABI
+void set_last_error(const std::string& msg);
+template <typename F>
+int guarded(F f) {
+  try {
+    f();
+    return TAWPIPE_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return TAWPIPE_ERUNTIME;
+  }
+}
 
 }  // namespace tp

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <string>
 #include <vector>
 
@@ -121,6 +122,8 @@ struct Ctx {
   std::vector<void*> dhb;  // m: gradient of the residual stream per micro-batch
   void *dY = nullptr, *dGU = nullptr, *db = nullptr, *dh1 = nullptr, *dO = nullptr, *dqkv = nullptr, *da = nullptr;
   float *delta = nullptr, *dq_acc = nullptr;
+  void* emb_scratch = nullptr;  // deterministic embedding backward: sort keys / positions + CUB temp
+  size_t emb_scratch_bytes = 0;
   void *fnorm = nullptr, *logits = nullptr, *df = nullptr;
   float *rstd_f = nullptr, *loss_rows = nullptr;
   int64_t Tc = 0;
@@ -146,6 +149,9 @@ struct Ctx {
 
 Ctx* g = nullptr;
 thread_local std::string g_err = "no error";
+}  // namespace
+void set_last_error(const std::string& msg) { g_err = msg; }
+namespace {
 
 void* dmalloc(size_t bytes) {
   void* p = nullptr;
@@ -194,13 +200,20 @@ struct Timed {  // RAII CUDA-event bracket on a stream (only when timing is enab
     r.stream = st == g->cs ? 0 : st == g->ws ? 1 : 2;
     TP_CUDA(cudaEventRecord(r.a, s));
   }
-  ~Timed() noexcept(false) {
+  // never throws: a destructor that runs while an exception unwinds must not raise a second one (that would
+  // terminate the process instead of returning TAWPIPE_ERUNTIME); a failed record is kept in g_err and the
+  // region is dropped
+  ~Timed() noexcept {
     if (trace_on()) {
-      TP_CUDA(cudaDeviceSynchronize());
-      TRACE("region kind %d done\n", r.kind);
+      const cudaError_t e = cudaDeviceSynchronize();
+      TRACE("region kind %d done (%s)\n", r.kind, cudaGetErrorString(e));
     }
-    if (!on) return;
-    TP_CUDA(cudaEventRecord(r.b, s));
+    if (!on || std::uncaught_exceptions() > 0) return;
+    const cudaError_t e = cudaEventRecord(r.b, s);
+    if (e != cudaSuccess) {
+      g_err = std::string("CUDA: ") + cudaGetErrorString(e) + " recording a timing event";
+      return;
+    }
     g->regions.push_back(r);
   }
 };
@@ -447,6 +460,7 @@ void gather(int uid, void* dst) {
 
 // a8 + a9: reduce-scatter in the group, rail P2P to the owner, ascending-k accumulate + AdamW, on gs
 void adam_update(const Unit& u, const void* const* contrib, int n_contrib, int own_k, bool own_f32);
+void adam_apply(const Unit& u, const GradSources& src, int n_src);
 
 // WeiPipe-style ring reduction: owner+1 starts the partial sum, each device adds its local fp32 gradient and
 // forwards it (wire dtype), the owner adds its own and applies AdamW
@@ -564,9 +578,20 @@ void reduce_and_update(int uid, float* gacc) {
   adam_update(u, contrib, g->D, g->k, own_f32);
 }
 
-// a9: fused accumulate of the group contributions (ascending order) + AdamW on this rank's owned stripe, on gs
+// a9: fused accumulate of the group contributions (ascending order) + AdamW on this rank's owned stripe, on gs.
+// contrib[kk] is group kk's contribution (one source per group on the NCCL paths); own_k's may be fp32.
 void adam_update(const Unit& u, const void* const* contrib, int n_contrib, int own_k, bool own_f32) {
-  cudaStream_t s = g->gs;
+  GradSources src;
+  src.n_groups = n_contrib;
+  for (int kk = 0; kk < n_contrib; ++kk) {
+    src.p[kk] = contrib[kk];
+    src.group_end[kk] = kk + 1;
+    if (kk == own_k && own_f32) src.f32_mask |= 1u << kk;
+  }
+  adam_apply(u, src, n_contrib);
+}
+
+AdamParams adam_params() {
   AdamParams hp;
   hp.lr = g->dims.lr;
   hp.beta1 = g->dims.beta1;
@@ -575,12 +600,24 @@ void adam_update(const Unit& u, const void* const* contrib, int n_contrib, int o
   hp.wd = g->dims.weight_decay;
   hp.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta1), g->step_t));
   hp.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(g->dims.beta2), g->step_t));
-  const int64_t stripe_off = u.lo;
-  Timed t(s, 2, (2.0 * n_contrib * g->esz + 26.0) * u.s);
-  BY_TYPE(adamw_fused<float>(contrib, n_contrib, own_k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
-                             (float*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s),
-          adamw_fused<bf16>(contrib, n_contrib, own_k, own_f32, g->master + u.off, g->mom + u.off, g->vel + u.off,
-                            (bf16*)wptr(g->wire, u.off), u.s, stripe_off, u.nd_lo, u.nd_hi, u.n_nd, hp, s));
+  return hp;
+}
+
+void adam_apply(const Unit& u, const GradSources& src, int n_src) {
+  cudaStream_t s = g->gs;
+  AdamRanges nd;
+  for (int r = 0; r < u.n_nd; ++r) {
+    nd.lo[r] = u.nd_lo[r];
+    nd.hi[r] = u.nd_hi[r];
+  }
+  // algorithmic bytes: the sources (fp32 4 B or wire) + master/m/v read 12 B + master/m/v/wire written 12 B + esz
+  double src_bytes = 0;
+  for (int si = 0; si < n_src; ++si) src_bytes += (src.f32_mask >> si & 1u) ? 4.0 : static_cast<double>(g->esz);
+  Timed t(s, 2, (src_bytes + 24.0 + g->esz) * u.s);
+  BY_TYPE(adamw_grouped<float>(src, g->master + u.off, g->mom + u.off, g->vel + u.off, (float*)wptr(g->wire, u.off),
+                               u.s, u.lo, nd, adam_params(), s),
+          adamw_grouped<bf16>(src, g->master + u.off, g->mom + u.off, g->vel + u.off, (bf16*)wptr(g->wire, u.off),
+                              u.s, u.lo, nd, adam_params(), s));
 }
 
 void wait_on(cudaStream_t s, cudaEvent_t e) {
@@ -932,7 +969,8 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   TP_CUDA(cudaMemsetAsync(c.gaccE, 0, c.units[E].n_pad * 4, c.cs));
   for (int mb = 0; mb < c.m; ++mb) {
     Timed t(c.cs, 4, 0);
-    embed_bwd(c.d_in + static_cast<int64_t>(mb) * c.T, c.S, c.Bm, c.S, c.dhb[mb], !c.bf, c.H, c.gaccE, c.cs);
+    embed_bwd(c.d_in + static_cast<int64_t>(mb) * c.T, c.S, c.Bm, c.S, c.dhb[mb], !c.bf, c.H, c.V, c.gaccE,
+              c.emb_scratch, c.emb_scratch_bytes, c.cs);
   }
   TP_CUDA(cudaEventRecord(c.evGE, c.cs));
   TP_CUDA(cudaStreamWaitEvent(c.gs, c.evGE, 0));
@@ -1179,8 +1217,10 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   c.dO = dmalloc(T * H * esz);
   c.dqkv = dmalloc(T * 3 * H * esz);
   c.da = dmalloc(T * H * esz);
-  c.delta = (float*)dmalloc(T * c.nh * 4);
+  c.delta = (float*)dmalloc(2 * T * c.nh * 4);   // δ, then the log2-domain LSE of the tcgen05 backward
   c.dq_acc = c.bf ? (float*)dmalloc(T * H * 4) : nullptr;
+  c.emb_scratch_bytes = embed_bwd_scratch_bytes(T);
+  c.emb_scratch = dmalloc(c.emb_scratch_bytes);
   c.Tc = std::min<int64_t>(T, 8192);
   c.fnorm = dmalloc(T * H * esz);
   c.df = dmalloc(T * H * esz);
@@ -1196,15 +1236,8 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   TP_CUDA(cudaMallocHost(&c.h_tok, tok_elems * 4));
   // RoPE tables in fp64 on the host, stored fp32 (R13)
   {
-    const int half = c.dh / 2;
-    std::vector<float> cs(static_cast<size_t>(c.S) * half), sn(cs.size());
-    for (int p = 0; p < c.S; ++p)
-      for (int i = 0; i < half; ++i) {
-        const double inv = std::pow(static_cast<double>(d->rope_theta), -2.0 * i / c.dh);
-        const double ang = static_cast<double>(p) * inv;
-        cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(ang));
-        sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(ang));
-      }
+    std::vector<float> cs, sn;
+    rope_tables_host(c.S, c.dh, d->rope_theta, cs, sn);
     c.cosT = (float*)dmalloc(cs.size() * 4);
     c.sinT = (float*)dmalloc(sn.size() * 4);
     TP_CUDA(cudaMemcpyAsync(c.cosT, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c.cs));
@@ -1298,20 +1331,6 @@ void destroy() {
   if (g->gs) cudaStreamDestroy(g->gs);
   delete g;
   g = nullptr;
-}
-
-template <typename F>
-int guarded(F f) {
-  try {
-    f();
-    return TAWPIPE_OK;
-  } catch (const Error& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return TAWPIPE_ERUNTIME;
-  }
 }
 
 }  // namespace
@@ -1513,54 +1532,5 @@ int tawpipe_set_link_emulation(double inter_gbps, double latency_us, int node_si
 const char* tawpipe_last_error(void) { return g_err.c_str(); }
 
 void tawpipe_finalize(void) { destroy(); }
-
-int tawpipe_gemm(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t a_ld, int a_kmajor, const void* B,
-                 int64_t b_ld, int b_kmajor, void* C, int64_t c_ld, int c_f32, int accumulate, const void* R,
-                 void* stream) {
-  return guarded([&] {
-    GemmArgs a{M, N, K, A, a_ld, a_kmajor != 0, B, b_ld, b_kmajor != 0, C, c_ld, c_f32 != 0, accumulate != 0, R};
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (dtype == TAWPIPE_BF16) {
-      const char* e = std::getenv("TAWPIPE_GEMM");
-      if (e && std::string(e) == "simt")
-        gemm_simt<bf16>(a, s);
-      else
-        gemm_tc_bf16(a, s);
-    } else if (dtype == TAWPIPE_FP32) {
-      gemm_simt<float>(a, s);
-    } else {
-      throw Error(TAWPIPE_ECONFIG, "bad dtype");
-    }
-  });
-}
-
-int tawpipe_attention_fwd(int dtype, int B, int S, int n_h, int d_h, const void* qkv, void* o, float* lse,
-                          void* stream) {
-  return guarded([&] {
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (dtype == TAWPIPE_FP32)
-      attention_fwd_simt<float>(B, S, n_h, d_h, (const float*)qkv, (float*)o, lse, s);
-    else if (attention_tc_supported(S, d_h) && !(std::getenv("TAWPIPE_ATTN") && std::string(std::getenv("TAWPIPE_ATTN")) == "simt"))
-      attention_fwd_tc(B, S, n_h, d_h, (const bf16*)qkv, (bf16*)o, lse, s);
-    else
-      attention_fwd_simt<bf16>(B, S, n_h, d_h, (const bf16*)qkv, (bf16*)o, lse, s);
-  });
-}
-
-int tawpipe_attention_bwd(int dtype, int B, int S, int n_h, int d_h, const void* qkv, const void* o, const float* lse,
-                          const void* do_, void* dqkv, float* delta, float* dq_acc, void* stream) {
-  return guarded([&] {
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (dtype == TAWPIPE_FP32)
-      attention_bwd_simt<float>(B, S, n_h, d_h, (const float*)qkv, (const float*)o, lse, (const float*)do_,
-                                (float*)dqkv, delta, s);
-    else if (attention_tc_supported(S, d_h) && !(std::getenv("TAWPIPE_ATTN") && std::string(std::getenv("TAWPIPE_ATTN")) == "simt"))
-      attention_bwd_tc(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv, delta,
-                       dq_acc, s);
-    else
-      attention_bwd_simt<bf16>(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv,
-                               delta, s);
-  });
-}
 
 }  // extern "C"

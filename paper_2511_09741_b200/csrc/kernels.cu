@@ -2,7 +2,9 @@
 // initialisation and the fused gradient-accumulate + AdamW update on the owned DBS stripe.
 // Formulas: SURVEY.md §8(c) (forward algorithm and backward-formula table); AdamW: PyTorch semantics (R1).
 // All reductions run in fp32 regardless of the storage type T (float or bf16).
+#include <cmath>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 
@@ -59,15 +61,6 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, int64_t stride
   const int b = static_cast<int>(row / S), p = static_cast<int>(row % S);
   const int64_t t = tok[b * stride_seq + p];
   for (int c = threadIdx.x; c < H; c += blockDim.x) h[row * H + c] = E[t * H + c];
-}
-
-template <typename T>
-__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, int64_t stride_seq, int S, const T* __restrict__ dh,
-                                 int H, float* __restrict__ dE) {
-  const int64_t row = blockIdx.x;
-  const int b = static_cast<int>(row / S), p = static_cast<int>(row % S);
-  const int64_t t = tok[b * stride_seq + p];
-  for (int c = threadIdx.x; c < H; c += blockDim.x) atomicAdd(&dE[t * H + c], to_f(dh[row * H + c]));
 }
 
 // ------------------------------------------------------------------------------------ RMSNorm
@@ -265,78 +258,98 @@ __global__ void init_normal_kernel(T* __restrict__ wire, float* __restrict__ mas
   }
 }
 
-// ------------------------------------------------------------------------------------ fused AdamW (a9)
-struct Contribs {
-  const void* p[8];
-};
+// ------------------------------------------------------------------------------------ fused accumulate + AdamW (a9)
+// g = Σ_groups (Σ_members src) in fp32: each group's sources are summed in member order into a partial, the partials
+// are added in ascending group order (R16); a source is fp32 (an fp32 gradient accumulator, possibly a peer's,
+// read over NVLink through its IPC mapping) or the wire dtype W (a group partial received on the rail).  Then
+// AdamW, PyTorch semantics (R1), on the owned stripe: master, m, v updated in place and the wire copy rewritten.
+__device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+__device__ __forceinline__ void st8f(float* p, const float (&f)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
+}
+__device__ __forceinline__ void ld8w(const float* p, float (&f)[8]) { ld8f(p, f); }
+__device__ __forceinline__ void ld8w(const bf16* p, float (&f)[8]);
+__device__ __forceinline__ void st8w(float* p, const float (&f)[8]) { st8f(p, f); }
+__device__ __forceinline__ void st8w(bf16* p, const float (&f)[8]);
 
+__device__ __forceinline__ bool no_decay(int64_t pos, const AdamRanges& r) {
+  return (pos >= r.lo[0] && pos < r.hi[0]) || (pos >= r.lo[1] && pos < r.hi[1]);
+}
+
+__device__ __forceinline__ void adamw_elem(float g, float& th, float& m, float& v, bool decay, const AdamParams& hp) {
+  if (decay) th *= 1.f - hp.lr * hp.wd;
+  m = hp.beta1 * m + (1.f - hp.beta1) * g;
+  v = hp.beta2 * v + (1.f - hp.beta2) * g * g;
+  th -= hp.lr * (m / hp.bc1) / (sqrtf(v / hp.bc2) + hp.eps);
+}
+
+// 8 elements per thread, 16-byte accesses (n % 8 == 0, 32-byte aligned fp32 / 16-byte aligned W stripes)
 template <typename W>
-__global__ void adamw_kernel(Contribs c, int n_contrib, int own_k, int own_f32, float* __restrict__ master,
-                             float* __restrict__ m, float* __restrict__ v, W* __restrict__ wire, int64_t n,
-                             int64_t unit_off, int64_t nd0_lo, int64_t nd0_hi, int64_t nd1_lo, int64_t nd1_hi,
-                             AdamParams hp) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float g = 0.f;
-    for (int k = 0; k < n_contrib; ++k) {  // ascending group index (R16)
-      if (k == own_k && own_f32)
-        g += static_cast<const float*>(c.p[k])[i];
-      else
-        g += to_f(static_cast<const W*>(c.p[k])[i]);
+__global__ void __launch_bounds__(256) adamw_grouped_v8_kernel(GradSources src, float* __restrict__ master,
+                                                               float* __restrict__ m, float* __restrict__ v,
+                                                               W* __restrict__ wire, int64_t n, int64_t unit_off,
+                                                               AdamRanges nd, AdamParams hp) {
+  const int64_t n8 = n / 8;
+  for (int64_t i8 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i8 < n8;
+       i8 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = i8 * 8;
+    float tot[8];
+    int s0 = 0;
+    for (int gi = 0; gi < src.n_groups; ++gi) {
+      float part[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int si = s0; si < src.group_end[gi]; ++si) {   // member order
+        float x[8];
+        if (src.f32_mask >> si & 1u)
+          ld8f(static_cast<const float*>(src.p[si]) + i, x);
+        else
+          ld8w(static_cast<const W*>(src.p[si]) + i, x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) part[e] += x[e];
+      }
+      s0 = src.group_end[gi];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) tot[e] = gi == 0 ? part[e] : tot[e] + part[e];   // ascending group order
     }
-    const int64_t pos = unit_off + i;
-    const bool decay = !((pos >= nd0_lo && pos < nd0_hi) || (pos >= nd1_lo && pos < nd1_hi));
-    float th = master[i];
-    if (decay) th *= 1.f - hp.lr * hp.wd;
-    const float mi = hp.beta1 * m[i] + (1.f - hp.beta1) * g;
-    const float vi = hp.beta2 * v[i] + (1.f - hp.beta2) * g * g;
-    const float denom = sqrtf(vi / hp.bc2) + hp.eps;
-    th -= hp.lr * (mi / hp.bc1) / denom;
-    master[i] = th;
-    m[i] = mi;
-    v[i] = vi;
-    wire[i] = from_f<W>(th);
+    float th[8], mm[8], vv[8];
+    ld8f(master + i, th);
+    ld8f(m + i, mm);
+    ld8f(v + i, vv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) adamw_elem(tot[e], th[e], mm[e], vv[e], !no_decay(unit_off + i + e, nd), hp);
+    st8f(master + i, th);
+    st8f(m + i, mm);
+    st8f(v + i, vv);
+    st8w(wire + i, th);
   }
 }
 
-// 4 elements per thread, 16-byte accesses to master/m/v (n % 4 == 0, 16-byte aligned stripes)
+// any n, any alignment
 template <typename W>
-__global__ void adamw_v4_kernel(Contribs c, int n_contrib, int own_k, int own_f32, float* __restrict__ master,
-                                float* __restrict__ m, float* __restrict__ v, W* __restrict__ wire, int64_t n,
-                                int64_t unit_off, int64_t nd0_lo, int64_t nd0_hi, int64_t nd1_lo, int64_t nd1_hi,
-                                AdamParams hp) {
-  const int64_t n4 = n / 4;
-  for (int64_t i4 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i4 < n4;
-       i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = i4 * 4;
-    float g[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k = 0; k < n_contrib; ++k) {  // ascending group index (R16)
-      if (k == own_k && own_f32) {
-        const float4 x = reinterpret_cast<const float4*>(c.p[k])[i4];
-        g[0] += x.x; g[1] += x.y; g[2] += x.z; g[3] += x.w;
-      } else {
-        const W* src = static_cast<const W*>(c.p[k]) + i;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) g[e] += to_f(src[e]);
-      }
+__global__ void adamw_grouped_kernel(GradSources src, float* __restrict__ master, float* __restrict__ m,
+                                     float* __restrict__ v, W* __restrict__ wire, int64_t n, int64_t unit_off,
+                                     AdamRanges nd, AdamParams hp) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float tot = 0.f;
+    int s0 = 0;
+    for (int gi = 0; gi < src.n_groups; ++gi) {
+      float part = 0.f;
+      for (int si = s0; si < src.group_end[gi]; ++si)
+        part += (src.f32_mask >> si & 1u) ? static_cast<const float*>(src.p[si])[i]
+                                          : to_f(static_cast<const W*>(src.p[si])[i]);
+      s0 = src.group_end[gi];
+      tot = gi == 0 ? part : tot + part;
     }
-    float4 th4 = reinterpret_cast<float4*>(master)[i4];
-    float4 m4 = reinterpret_cast<float4*>(m)[i4];
-    float4 v4 = reinterpret_cast<float4*>(v)[i4];
-    float th[4] = {th4.x, th4.y, th4.z, th4.w}, mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t pos = unit_off + i + e;
-      const bool decay = !((pos >= nd0_lo && pos < nd0_hi) || (pos >= nd1_lo && pos < nd1_hi));
-      if (decay) th[e] *= 1.f - hp.lr * hp.wd;
-      mm[e] = hp.beta1 * mm[e] + (1.f - hp.beta1) * g[e];
-      vv[e] = hp.beta2 * vv[e] + (1.f - hp.beta2) * g[e] * g[e];
-      th[e] -= hp.lr * (mm[e] / hp.bc1) / (sqrtf(vv[e] / hp.bc2) + hp.eps);
-      wire[i + e] = from_f<W>(th[e]);
-    }
-    reinterpret_cast<float4*>(master)[i4] = make_float4(th[0], th[1], th[2], th[3]);
-    reinterpret_cast<float4*>(m)[i4] = make_float4(mm[0], mm[1], mm[2], mm[3]);
-    reinterpret_cast<float4*>(v)[i4] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    float th = master[i], mm = m[i], vv = v[i];
+    adamw_elem(tot, th, mm, vv, !no_decay(unit_off + i, nd), hp);
+    master[i] = th;
+    m[i] = mm;
+    v[i] = vv;
+    wire[i] = from_f<W>(th);
   }
 }
 
@@ -359,6 +372,8 @@ __device__ __forceinline__ void st8(bf16* p, const float (&f)[8]) {
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = u;
 }
+__device__ __forceinline__ void ld8w(const bf16* p, float (&f)[8]) { ld8(p, f); }
+__device__ __forceinline__ void st8w(bf16* p, const float (&f)[8]) { st8(p, f); }
 
 // grid (rows), block = nblk·nh·(half/8) threads (<= 1024): each thread rotates 8 pairs of one head
 __global__ void rope_v8_kernel(bf16* __restrict__ qkv, int S, int nh, int dh, int64_t ld, const float* __restrict__ cs,
@@ -586,16 +601,6 @@ void embed_fwd(const int32_t* tok, int64_t stride_seq, int B, int S, const T* E,
   embed_fwd_kernel<T><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S, E, H, h);
   LAUNCHED();
 }
-void embed_bwd(const int32_t* tok, int64_t stride_seq, int B, int S, const void* dh, bool dh_f32, int H, float* dE,
-               cudaStream_t s) {
-  if (dh_f32)
-    embed_bwd_kernel<float><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S,
-                                                                          static_cast<const float*>(dh), H, dE);
-  else
-    embed_bwd_kernel<bf16><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S,
-                                                                         static_cast<const bf16*>(dh), H, dE);
-  LAUNCHED();
-}
 template <typename T>
 void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
   if constexpr (std::is_same<T, bf16>::value) {
@@ -733,20 +738,21 @@ void init_normal(T* wire, float* master, int64_t n, int64_t global_off, uint64_t
   LAUNCHED();
 }
 template <typename W>
-void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_f32, float* master, float* m, float* v,
-                 W* wire, int64_t n, int64_t unit_off, const int64_t* nd_lo, const int64_t* nd_hi, int n_nd,
-                 AdamParams p, cudaStream_t s) {
-  TP_CHECK(n_contrib >= 1 && n_contrib <= 8, TAWPIPE_ECONFIG, "adamw: 1..8 group contributions supported");
-  Contribs c{};
-  for (int k = 0; k < n_contrib; ++k) c.p[k] = contrib[k];
-  const int64_t l0 = n_nd > 0 ? nd_lo[0] : 0, h0 = n_nd > 0 ? nd_hi[0] : 0;
-  const int64_t l1 = n_nd > 1 ? nd_lo[1] : 0, h1 = n_nd > 1 ? nd_hi[1] : 0;
-  if (n % 4 == 0)
-    adamw_v4_kernel<W><<<grid_stride_blocks(n / 4), 256, 0, s>>>(c, n_contrib, own_k, own_f32 ? 1 : 0, master, m, v,
-                                                                 wire, n, unit_off, l0, h0, l1, h1, p);
+void adamw_grouped(const GradSources& src, float* master, float* m, float* v, W* wire, int64_t n, int64_t unit_off,
+                   const AdamRanges& nd, const AdamParams& p, cudaStream_t s) {
+  TP_CHECK(src.n_groups >= 1 && src.n_groups <= 8 && src.group_end[src.n_groups - 1] <= 16, TAWPIPE_ECONFIG,
+           "adamw: 1..8 groups and at most 16 gradient sources");
+  for (int gi = 0; gi < src.n_groups; ++gi)
+    TP_CHECK(src.group_end[gi] > (gi ? src.group_end[gi - 1] : 0), TAWPIPE_ECONFIG, "adamw: empty source group");
+  if (n <= 0) return;
+  bool vec = n % 8 == 0 && reinterpret_cast<uintptr_t>(master) % 32 == 0 && reinterpret_cast<uintptr_t>(m) % 32 == 0 &&
+             reinterpret_cast<uintptr_t>(v) % 32 == 0 && reinterpret_cast<uintptr_t>(wire) % 16 == 0;
+  for (int si = 0; si < src.group_end[src.n_groups - 1]; ++si)
+    vec = vec && reinterpret_cast<uintptr_t>(src.p[si]) % ((src.f32_mask >> si & 1u) ? 32 : 16) == 0;
+  if (vec)
+    adamw_grouped_v8_kernel<W><<<grid_stride_blocks(n / 8), 256, 0, s>>>(src, master, m, v, wire, n, unit_off, nd, p);
   else
-    adamw_kernel<W><<<grid_stride_blocks(n), 256, 0, s>>>(c, n_contrib, own_k, own_f32 ? 1 : 0, master, m, v, wire, n,
-                                                          unit_off, l0, h0, l1, h1, p);
+    adamw_grouped_kernel<W><<<grid_stride_blocks(n), 256, 0, s>>>(src, master, m, v, wire, n, unit_off, nd, p);
   LAUNCHED();
 }
 
@@ -763,8 +769,8 @@ void adamw_fused(const void* const* contrib, int n_contrib, int own_k, bool own_
   template void cast_to_f32<T>(const T*, float*, int64_t, cudaStream_t);                                         \
   template void add_cast<T>(const T*, const float*, T*, int64_t, cudaStream_t);                                  \
   template void init_normal<T>(T*, float*, int64_t, int64_t, uint64_t, float, cudaStream_t);                     \
-  template void adamw_fused<T>(const void* const*, int, int, bool, float*, float*, float*, T*, int64_t, int64_t, \
-                               const int64_t*, const int64_t*, int, AdamParams, cudaStream_t);
+  template void adamw_grouped<T>(const GradSources&, float*, float*, float*, T*, int64_t, int64_t,               \
+                                 const AdamRanges&, const AdamParams&, cudaStream_t);
 INST(float)
 INST(bf16)
 
@@ -785,4 +791,18 @@ void link_delay(double seconds, cudaStream_t s) {
   g_kstats.launches++;
 }
 
+}  // namespace tp
+
+namespace tp {
+void rope_tables_host(int S, int dh, double theta, std::vector<float>& cos_t, std::vector<float>& sin_t) {
+  const int half = dh / 2;
+  cos_t.assign(static_cast<size_t>(S) * half, 0.f);
+  sin_t.assign(static_cast<size_t>(S) * half, 0.f);
+  for (int p = 0; p < S; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double ang = static_cast<double>(p) * std::pow(theta, -2.0 * i / dh);
+      cos_t[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(ang));
+      sin_t[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(ang));
+    }
+}
 }  // namespace tp

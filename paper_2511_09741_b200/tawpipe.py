@@ -76,6 +76,17 @@ def lib():
         "tawpipe_gemm": (i32, [i32, i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, vp, vp]),
         "tawpipe_attention_fwd": (i32, [i32, i32, i32, i32, i32, vp, vp, vp, vp]),
         "tawpipe_attention_bwd": (i32, [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "tawpipe_gemm_swiglu": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tawpipe_gemm_swiglu_bwd": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tawpipe_rmsnorm_fwd": (i32, [i32, i64, i32, vp, vp, f32, vp, vp, vp]),
+        "tawpipe_rmsnorm_bwd": (i32, [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "tawpipe_rope": (i32, [i32, i32, i32, i32, i32, f32, vp, i32, vp]),
+        "tawpipe_swiglu_fwd": (i32, [i32, i64, i32, vp, vp, vp]),
+        "tawpipe_swiglu_bwd": (i32, [i32, i64, i32, vp, vp, vp, vp]),
+        "tawpipe_cross_entropy": (i32, [i32, i64, i32, vp, vp, f32, vp, vp]),
+        "tawpipe_embed_fwd": (i32, [i32, i32, i32, vp, i64, vp, i32, vp, vp]),
+        "tawpipe_embed_bwd": (i32, [i32, i32, i32, vp, i64, vp, i32, i32, vp, vp]),
+        "tawpipe_adamw": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -270,5 +281,60 @@ def attention_fwd(dtype, B, S, nh, dh, qkv, o, lse, stream=None):
     _check(lib().tawpipe_attention_fwd(dtype, B, S, nh, dh, qkv, o, lse, stream))
 
 
-def attention_bwd(dtype, B, S, nh, dh, qkv, o, lse, do, dqkv, delta, dq_acc, stream=None):
-    _check(lib().tawpipe_attention_bwd(dtype, B, S, nh, dh, qkv, o, lse, do, dqkv, delta, dq_acc, stream))
+def attention_bwd(dtype, B, S, nh, dh, qkv, o, lse, do, dqkv, scratch, dq_acc, stream=None):
+    """scratch: 2·B·n_h·S fp32 (δ and the log2-domain LSE)."""
+    _check(lib().tawpipe_attention_bwd(dtype, B, S, nh, dh, qkv, o, lse, do, dqkv, scratch, dq_acc, stream))
+
+
+def gemm_swiglu(M, I, K, x, w_gu, gu, y, stream=None):
+    _check(lib().tawpipe_gemm_swiglu(M, I, K, x, w_gu, gu, y, stream))
+
+
+def gemm_swiglu_bwd(M, I, K, dh, w_down, gu, dgu, stream=None):
+    _check(lib().tawpipe_gemm_swiglu_bwd(M, I, K, dh, w_down, gu, dgu, stream))
+
+
+def rmsnorm_fwd(dtype, rows, H, x, gamma, eps, y, rstd, stream=None):
+    _check(lib().tawpipe_rmsnorm_fwd(dtype, rows, H, x, gamma, eps, y, rstd, stream))
+
+
+def rmsnorm_bwd(dtype, rows, H, dy, x, gamma, rstd, res, dx, dgamma_acc, stream=None):
+    _check(lib().tawpipe_rmsnorm_bwd(dtype, rows, H, dy, x, gamma, rstd, res, dx, dgamma_acc, stream))
+
+
+def rope(dtype, B, S, nh, dh, theta, qkv, inverse, stream=None):
+    _check(lib().tawpipe_rope(dtype, B, S, nh, dh, theta, qkv, int(inverse), stream))
+
+
+def swiglu_fwd(dtype, rows, I, gu, y, stream=None):
+    _check(lib().tawpipe_swiglu_fwd(dtype, rows, I, gu, y, stream))
+
+
+def swiglu_bwd(dtype, rows, I, dy, gu, dgu, stream=None):
+    _check(lib().tawpipe_swiglu_bwd(dtype, rows, I, dy, gu, dgu, stream))
+
+
+def cross_entropy(dtype, rows, V, logits, targets, inv_denom, loss_rows, stream=None):
+    _check(lib().tawpipe_cross_entropy(dtype, rows, V, logits, targets, inv_denom, loss_rows, stream))
+
+
+def embed_fwd(dtype, B, S, tokens, tok_stride, E, H, h, stream=None):
+    _check(lib().tawpipe_embed_fwd(dtype, B, S, tokens, tok_stride, E, H, h, stream))
+
+
+def embed_bwd(dtype, B, S, tokens, tok_stride, dh, H, V, dE, stream=None):
+    _check(lib().tawpipe_embed_bwd(dtype, B, S, tokens, tok_stride, dh, H, V, dE, stream))
+
+
+def adamw(wire_dtype, groups, master, m, v, wire, n, unit_off=0, no_decay=None, lr=1e-3, beta1=0.9, beta2=0.95,
+          eps=1e-8, wd=0.1, step=1, stream=None):
+    """groups: list of groups, each a list of (device pointer, is_f32) sources summed in member order, the groups in
+    list order (tawpipe_adamw)."""
+    sizes = (ctypes.c_int * len(groups))(*[len(gr) for gr in groups])
+    flat = [src for gr in groups for src in gr]
+    ptrs = (ctypes.c_void_p * len(flat))(*[p for p, _ in flat])
+    f32 = (ctypes.c_int * len(flat))(*[int(bool(f)) for _, f in flat])
+    nd = None if no_decay is None else (ctypes.c_int64 * 4)(*no_decay)
+    hyper = (ctypes.c_float * 5)(lr, beta1, beta2, eps, wd)
+    _check(lib().tawpipe_adamw(wire_dtype, len(groups), sizes, ptrs, f32, master, m, v, wire, n, unit_off, nd, hyper,
+                               step, stream))

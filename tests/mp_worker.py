@@ -29,15 +29,17 @@ def main():
     ap.add_argument("--literal", action="store_true")
     ap.add_argument("--emu-gbps", type=float, default=0.0)   # NEXT-3 emulated inter-node link
     ap.add_argument("--emu-node", type=int, default=0)
+    ap.add_argument("--linear", action="store_true", help="AdamW ε = 1, lr = 1, no decay: update linear in g (R18)")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
-    cfg = oracle_cfg(json.loads(a.cfg))
+    hyper = dict(lr=1.0, adam_eps=1.0, weight_decay=0.0) if a.linear else {}
+    cfg = oracle_cfg(json.loads(a.cfg), **hyper)
     rank, world, local = T.bootstrap()
     params = synth.perturb_gains(synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab))
     dims = T.ModelDims(n_layers=cfg.n_layers, hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, vocab=cfg.vocab,
                        seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=a.dtype, ckpt=a.ckpt,
                        schedule=(T.NO_CCO if a.no_cco else T.GWPS) | (T.RING if a.ring else 0)
-                       | (T.LITERAL if a.literal else 0))
+                       | (T.LITERAL if a.literal else 0), **hyper)
     sess = T.Session(world, a.G, dims, a.N)
     sess.load(T.pack_full_model(params))
     if a.emu_gbps > 0:

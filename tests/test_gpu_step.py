@@ -1,6 +1,10 @@
 """Whole-step parity on one B200 through the C ABI: tawpipe_step vs the fp64 oracle's plain single-device
 AdamW step.  fp32 path: loss ≤ 1e-5, weights ≤ 1e-4; bf16 path: loss ≤ 1e-2, weights
-≤ 2e-2 (north_star tolerances, weight metric R18).  Steps 1 and 3."""
+≤ 2e-2 (north_star tolerances, weight metric R18).  Steps 1 and 3.
+
+R18: with the default AdamW ε = 1e-8 an update is ≈ −lr·sign(g) early on, so e_Δ cannot see a wrong
+gradient magnitude; the LINEAR cases therefore run AdamW with ε = 1 ≫ |g| (and no weight decay), where the update
+is ≈ −lr·m̂, linear in the gradient, and assert e_Δ at every step."""
 import numpy as np
 import pytest
 
@@ -27,13 +31,19 @@ def layer_fwd_flops(cfg, T_tok):
     return (2.0 * T_tok * 3 * H * H, 2.0 * H * (S + 1) * S * cfg.micro_bs, 2.0 * T_tok * H * H, 2.0 * T_tok * 2 * I * H)
 
 
-def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=3, gains=True, recompute=None):
-    cfg = oracle_cfg(base)
+LINEAR = dict(lr=1.0, adam_eps=1.0, weight_decay=0.0)   # AdamW update ≈ −m̂: linear in the gradient (R18)
+
+
+def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=3, gains=True, recompute=None,
+               hyper=None):
+    hyper = hyper or {}
+    linear = hyper.get("adam_eps", 1e-8) >= 1e-3
+    cfg = oracle_cfg(base, **hyper)
     params = synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab)
     if gains:
         params = synth.perturb_gains(params)
     dims = T.ModelDims(n_layers=cfg.n_layers, hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, vocab=cfg.vocab,
-                       seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=dtype, ckpt=ckpt)
+                       seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=dtype, ckpt=ckpt, **hyper)
     sess = T.Session(1, 1, dims, n_micro)
     try:
         sess.load(T.pack_full_model(params))
@@ -49,14 +59,14 @@ def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=
             lr, grads = om.train_step(st, toks, cfg)
             grads_all.append(grads)
             assert abs(lg - lr) / abs(lr) <= tol_loss, (step, lg, lr)
-            if step in (0, steps - 1):
+            if step in (0, steps - 1) or linear:
                 gpu = reassemble(cfg, 1, 1, [sess.shard()])
                 et, ed, viol, off, rep = weight_errors(gpu, st.params, theta0, grads_all, cfg, kappa)
                 print(f"step {step + 1}: loss {lg:.7f} vs {lr:.7f}; e_theta {et:.2e} e_delta {ed:.2e} "
                       f"off-W {off:.3%} violations {viol}")
-                # e_Δ is the step-1 check (Δ = −lr(wd·θ + g/(|g|+ε)) is well conditioned there); later steps
-                # keep e_θ and the off-W bound, since AdamW's m/√v cancellation amplifies rounding (R18 reading)
-                assert et <= tol_w and (step > 0 or ed <= tol_w) and viol == 0, (
+                # e_Δ: every step in the linear cases; otherwise the step-1 check (Δ = −lr(wd·θ + g/(|g|+ε)) is
+                # well conditioned there; later AdamW's m/√v cancellation amplifies rounding, R18 reading)
+                assert et <= tol_w and ((step > 0 and not linear) or ed <= tol_w) and viol == 0, (
                     step, et, ed, viol, sorted(rep, key=lambda r: -max(r[1], r[2]))[:3])
         led = sess.ledger()
         assert all(x == 0 for x in led)   # P = 1: no communication at all
@@ -115,6 +125,32 @@ def test_c0b_bf16_partial_keep_step_matches_oracle(T, monkeypatch):
     n_rec = cfg.n_layers * 2 - 1
     run_parity(T, C0B, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=1, n_micro=2, steps=2,
                recompute=n_rec * mlp + (n_rec - 1) * o)
+
+
+def test_c0_fp32_linear_update_step_matches_oracle(T):
+    """ε = 1 ≫ |g|, no decay: e_Δ at every step sees any wrong per-tensor gradient magnitude."""
+    run_parity(T, C0, T.FP32, 1e-5, 1e-4, 1e-3, hyper=LINEAR)
+
+
+def test_c0b_bf16_linear_update_step_matches_oracle(T):
+    run_parity(T, C0B, T.BF16, 1e-2, 2e-2, 5e-2, n_micro=2, hyper=LINEAR)
+
+
+def test_c0b_bf16_linear_full_recompute_step_matches_oracle(T):
+    run_parity(T, C0B, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=2, n_micro=2, hyper=LINEAR)
+
+
+def test_bf16_h4096_step_matches_oracle(T):
+    """The C3 layer width (H = 4096, 32 heads of 128, I = 11008): the CTA-per-row RMSNorm kernels, the dγ column
+    reduction, rope_v8 with 32 heads and the tcgen05 GEMM shapes of the bench, in one whole step (L = 1, S = 256)."""
+    base = dict(n_layers=1, hidden=4096, heads=32, ffn=11008, vocab=512, seq=256, micro_bs=1)
+    run_parity(T, base, T.BF16, 1e-2, 2e-2, 5e-2, ckpt=1, n_micro=1, steps=2, hyper=LINEAR)
+
+
+def test_bf16_multichunk_head_step_matches_oracle(T):
+    """micro_bs·S = 10,240 > the head's 8,192-row chunk: two chunks, the second ragged (2,048 rows)."""
+    base = dict(C0B, n_layers=1, micro_bs=40)
+    run_parity(T, base, T.BF16, 1e-2, 2e-2, 5e-2, n_micro=1, steps=2, hyper=LINEAR)
 
 
 def test_trace_export_and_idle_fraction(T):

@@ -319,3 +319,35 @@ def test_model_sizes_match_paper():
     # exact φ = 4H² + 3HI + 2H reduces to 12H² + 2H when I = 8H/3 (H = 96, I = 256)
     cfg = om.ModelConfig(n_layers=1, hidden=96, heads=1, ffn=256, vocab=2, seq=1)
     assert om.phi(cfg) == 12 * 96 * 96 + 2 * 96
+
+
+def test_attention_row_block_and_key_row_forms_equal_matrix_form():
+    """oracle.attention_fwd_rows (a block of query rows) and oracle.attention_key_row (one key row of the backward,
+    used for the full-size dK / dV spot checks) agree with the pinned matrix forms; and independently of them the
+    key-row form satisfies the identities of the mathematics: Σ_j dK_j = 0 (each row of dS sums to
+    Σ_j P_ij dP_ij − δ_i = do_i·o_i − δ_i = 0), Σ_j dV_j = Σ_i do_i (rows of P sum to 1), and the last key is seen
+    by the last query only: dV_{S−1} = P_{S−1,S−1}·do_{S−1}."""
+    rng = np.random.default_rng(5)
+    S, nh, dh = 11, 2, 8
+    q, k, v, do = (rng.standard_normal((S, nh, dh)) for _ in range(4))
+    o, P = om.attention_fwd(q, k, v)
+    _, dk, dv = om.attention_bwd(do, q, k, v, o, P)
+    for h in range(nh):
+        ob, lb = om.attention_fwd_rows(3, 9, q[:, h], k[:, h], v[:, h])
+        np.testing.assert_allclose(ob, o[3:9, h], rtol=1e-12, atol=1e-14)
+        o_all, lse_all = om.attention_fwd_rows(0, S, q[:, h], k[:, h], v[:, h])
+        for i in (0, 4, S - 1):
+            _, lse_i, _ = om.attention_row(i, q[i, h], k[:, h], v[:, h], do[i, h])
+            assert abs(lse_all[i] - lse_i) < 1e-12
+        sk, sv = np.zeros(dh), np.zeros(dh)
+        for j in range(S):
+            dkj, dvj = om.attention_key_row(j, k[j, h], v[j, h], q[:, h], do[:, h], o_all, lse_all)
+            np.testing.assert_allclose(dkj, dk[j, h], rtol=1e-11, atol=1e-13)
+            np.testing.assert_allclose(dvj, dv[j, h], rtol=1e-11, atol=1e-13)
+            sk += dkj
+            sv += dvj
+        np.testing.assert_allclose(sk, 0.0, atol=1e-12)
+        np.testing.assert_allclose(sv, do[:, h].sum(0), rtol=1e-12, atol=1e-12)
+        _, dv_last = om.attention_key_row(S - 1, k[S - 1, h], v[S - 1, h], q[:, h], do[:, h], o_all, lse_all)
+        p_last = np.exp(q[S - 1, h] @ k[S - 1, h] / np.sqrt(dh) - lse_all[S - 1])
+        np.testing.assert_allclose(dv_last, p_last * do[S - 1, h], rtol=1e-13)

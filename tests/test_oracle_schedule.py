@@ -166,3 +166,44 @@ def test_striped_group_map_equals_paper_group_map_when_L_equals_P():
         own = routes.owner_table(P, D)
         for l in range(P):
             assert own[l] // G == l % D
+
+
+@pytest.mark.parametrize("P,L", [(2, 2), (3, 3), (4, 4), (4, 8), (5, 10), (8, 8)])
+def test_ring_ledger_sent_side_conservation_and_hop_count(P, L):
+    """Pins ring_ledger's SENT counters (the receive side is pinned by the 3L(P−1)φ/P identity): on a ring every
+    transfer is one hop, so summed over the P devices sent == received for every (kind, unit); and a gather
+    (reduction) of a unit of n elements moves it over exactly P − 1 ring edges, so the job-wide sent total is
+    (P − 1) × Σ n over the step's 2L − 1 + 2 gathers (L + 2 reductions)."""
+    s, e, f = 1000, 70, 90
+    leds = [LG.ring_ledger(L, P, d, s, e, f, r=1) for d in range(P)]
+    for kind in LG.KINDS:
+        for unit in LG.UNITS:
+            for cls in LG.CLASSES:
+                sent = sum(x[LG.index(kind, cls, "sent", unit)] for x in leds)
+                recv = sum(x[LG.index(kind, cls, "recv", unit)] for x in leds)
+                assert sent == recv, (kind, cls, unit, sent, recv)
+    n_gather = {"block": (2 * L - 1) * s, "E": e, "F": f}
+    n_reduce = {"block": L * s, "E": e, "F": f}
+    for unit in LG.UNITS:
+        assert sum(x[LG.index("w", "inter", "sent", unit)] for x in leds) == (P - 1) * n_gather[unit]
+        assert sum(x[LG.index("g", "inter", "sent", unit)] for x in leds) == (P - 1) * n_reduce[unit]
+        assert all(x[LG.index(k, "intra", dr, unit)] == 0 for x in leds for k in LG.KINDS for dr in LG.DIRS)
+
+
+@pytest.mark.parametrize("P,G,L", [(4, 2, 4), (6, 2, 6), (6, 3, 6), (8, 2, 8), (4, 4, 4), (4, 1, 4)])
+def test_gwps_and_literal_ledgers_conserve_every_transfer(P, G, L):
+    """Every logical transfer has one sender and one receiver: summed over the P devices, sent == received per
+    (kind, class, unit), for the striped closed forms (App. A) and for the paper-literal enumeration."""
+    D = P // G
+    s, e, f = 64 * G * 3, 64 * G, 64 * G * 2
+    striped = [LG.closed_form(L, P, G, d // G, s // G, e // G, f // G, r=1) for d in range(P)]
+    literal = [LG.literal_ledger(L, P, D, d, s, e, f, r=1) for d in range(P)] if L % P == 0 else []
+    for leds in (striped, literal):
+        if not leds:
+            continue
+        for kind in LG.KINDS:
+            for cls in LG.CLASSES:
+                for unit in LG.UNITS:
+                    sent = sum(x[LG.index(kind, cls, "sent", unit)] for x in leds)
+                    recv = sum(x[LG.index(kind, cls, "recv", unit)] for x in leds)
+                    assert sent == recv, (kind, cls, unit, sent, recv)

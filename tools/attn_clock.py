@@ -11,7 +11,7 @@ qkv = (torch.randn(S, 3 * H, device="cuda") * 0.5).bfloat16()
 do = torch.randn(S, H, device="cuda").bfloat16()
 o = torch.empty(S, H, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(nh, S, device="cuda")
-dqkv = torch.empty_like(qkv); delta = torch.empty(nh, S, device="cuda"); acc = torch.empty(S, H, device="cuda")
+dqkv = torch.empty_like(qkv); delta = torch.empty(2, nh, S, device="cuda"); acc = torch.empty(S, H, device="cuda")
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 fw, bw = [], []
 with ClockSampler(0) as clk:

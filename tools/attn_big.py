@@ -10,7 +10,7 @@ qkv = (torch.randn(S, 3 * H, device="cuda") * 0.5).bfloat16()
 do = torch.randn(S, H, device="cuda").bfloat16()
 o = torch.empty(S, H, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(nh, S, device="cuda")
-dqkv = torch.empty_like(qkv); delta = torch.empty(nh, S, device="cuda"); acc = torch.empty(S, H, device="cuda")
+dqkv = torch.empty_like(qkv); delta = torch.empty(2, nh, S, device="cuda"); acc = torch.empty(S, H, device="cuda")
 for it in range(3):
     torch.cuda.synchronize(); t0 = time.time()
     T.attention_fwd(T.BF16, 1, S, nh, dh, qkv.data_ptr(), o.data_ptr(), lse.data_ptr())

@@ -59,7 +59,7 @@ extern "C" {
                                    units.  Exclusive with TAWPIPE_RING; combinable with TAWPIPE_NO_CCO.  */
 
 #define TAWPIPE_LEDGER_N 24     /* see tawpipe_ledger */
-#define TAWPIPE_STATS_N  16     /* see tawpipe_stats  */
+#define TAWPIPE_STATS_N  19     /* see tawpipe_stats  */
 
 /* Model dimensions and hyper-parameters.  Symbols follow PAPER.md Table 1;
  * the rest are LLaMA-2 conventions. */
@@ -156,7 +156,10 @@ int tawpipe_ledger(uint64_t* out, int n);
  *  [9] AdamW ms   [10] AdamW algorithmic GB          [11] kernel launches in the step
  *  [12] peak device bytes allocated (GB)             [13] wire bytes per element
  *  [14] elementwise/norm ms
- *  [15] algorithmic GFLOP of the recompute passes (checkpointing) executed in the step   LOCAL. */
+ *  [15] algorithmic GFLOP of the recompute passes (checkpointing) executed in the step
+ *  [16] 1 if the step ran the NVLink peer path (IPC-mapped copies / peer loads), 0 for NCCL collectives
+ *  [17] GB of weight stripes this rank pulled over NVLink   [18] GB of gradients this rank's kernels read
+ *       over NVLink (fp32 group stripes + wire-dtype rail partials)                                LOCAL. */
 int tawpipe_stats(double* out, int n);
 
 /* Enable (1) / disable (0) per-kernel CUDA-event timing for tawpipe_stats.  LOCAL. */

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "peer.cuh"
 
 namespace tp {
 
@@ -133,6 +134,15 @@ struct Ctx {
   double* h_loss = nullptr;
   uint64_t ledger[TAWPIPE_LEDGER_N] = {};
   int step_t = 0;
+  // NVLink peer path of the GWPS schedule (peer.cu): IPC-mapped buffers of every rank, sequence flags
+  bool p2p = false;
+  std::vector<std::vector<void*>> peer;   // [rank][PB_*]
+  std::vector<int64_t> gofs;              // [group][unit]: offset of the unit's stripe in that group's owned arrays
+  uint32_t* sig = nullptr;                // this rank's flags [SK_*][source rank]
+  void* part = nullptr;                   // rail partials of this rank's group (4 slots: layer 0/1, E, F) × max_s
+  uint32_t wseq = 0, gseq = 0;            // gathers / reductions issued so far (identical on every rank)
+  uint32_t wprev[2] = {0, 0}, gprev[2] = {0, 0}, pprev[4] = {0, 0, 0, 0};
+  double nvl_w_bytes = 0, nvl_g_bytes = 0;   // bytes this rank pulled / read over NVLink in the last step
   // events
   cudaEvent_t w_ready[2], w_free[2], g_ready[2], g_free[2], evE, evF, evGF, evGE, ev_s0, ev_s1, ev_ws0, ev_ws1,
       ev_gs0, ev_gs1;
@@ -146,6 +156,11 @@ struct Ctx {
   std::vector<void*> allocs;
   long launches_at_start = 0;
 };
+
+// peer buffers (Ctx::peer[rank][PB_*]) and signal kinds (Ctx::sig[SK_* · kSigRanks + source rank])
+enum { PB_WIRE, PB_WBUF0, PB_WBUF1, PB_EBUF, PB_FBUF, PB_GACC0, PB_GACC1, PB_GACCE, PB_GACCF, PB_PART, PB_SIG, PB_N };
+enum { SK_RAIL, SK_WDONE, SK_GREADY, SK_GDONE, SK_PREADY, SK_PDONE, SK_N };
+constexpr int kSigRanks = 64;
 
 Ctx* g = nullptr;
 thread_local std::string g_err = "no error";
@@ -397,10 +412,18 @@ void* unit_buffer(int uid, int slot) {
   return g->wbuf[slot];
 }
 
+void gather_p2p(int uid, int slot);
+void reduce_p2p(int uid, int slot, float* gacc);
+
 // a3: rail P2P of stripe j from the owner group (if remote) + intra-group all-gather, on ws
-void gather(int uid, void* dst) {
+void gather(int uid, int slot) {
   const Unit& u = g->units[uid];
   if (g->P == 1) return;  // nothing to move; the compute reads the owned copy in place
+  if (g->p2p) {
+    gather_p2p(uid, slot);
+    return;
+  }
+  void* dst = unit_buffer(uid, slot);
   Timed t(g->ws, 5, 0);
   void* own = wptr(g->wire, u.off);
   if (g->ring) {  // owner -> owner+1 -> ... : receive from d-1, then forward to d+1 (stream-ordered)
@@ -498,8 +521,12 @@ void reduce_ring(const Unit& u, float* gacc) {
   ledger_reduce_ring(u, d, P, g->ledger);
 }
 
-void reduce_and_update(int uid, float* gacc) {
+void reduce_and_update(int uid, int slot, float* gacc) {
   const Unit& u = g->units[uid];
+  if (g->p2p) {
+    reduce_p2p(uid, slot, gacc);
+    return;
+  }
   if (g->ring) {
     reduce_ring(u, gacc);
     return;
@@ -618,6 +645,156 @@ void adam_apply(const Unit& u, const GradSources& src, int n_src) {
                                u.s, u.lo, nd, adam_params(), s),
           adamw_grouped<bf16>(src, g->master + u.off, g->mom + u.off, g->vel + u.off, (bf16*)wptr(g->wire, u.off),
                               u.s, u.lo, nd, adam_params(), s));
+}
+
+// ------------------------------------------------------------------------------------ NVLink peer path (GWPS)
+// Replaces the NCCL collectives of the striped schedule when every rank could map every peer (peer.cu):
+//   a3  rank (k, j) pulls stripe j of a remote unit from its owner (k_o, j)'s wire copy (the rail transfer), then
+//       the other G−1 stripes from its group members (from their wire copies when the group owns the unit, else
+//       from the slot each member filled over its own rail) -- plain cudaMemcpyAsync calls, run by copy engines;
+//   a8  the members' fp32 gradient accumulators are read in place over NVLink: a non-owner group's member j sums
+//       stripe j over its group into a wire-dtype rail partial; the owner's member j reads its group's G fp32
+//       stripes and the D−1 rail partials inside
+//   a9  the fused accumulate + AdamW kernel.
+// Every cross-rank dependency is a sequence flag (RAW: "ready", WAR: "done reading"); the step-end loss all-reduce
+// orders one step's owner updates before the next step's pulls.
+inline int rank_of(int k, int j) { return k * g->G + j; }
+inline uint32_t* flag_at(int dst_rank, int kind, int src_rank) {
+  return static_cast<uint32_t*>(g->peer[dst_rank][PB_SIG]) + kind * kSigRanks + src_rank;
+}
+inline const uint32_t* my_flag(int kind, int src_rank) { return g->sig + kind * kSigRanks + src_rank; }
+inline char* peer_ptr(int rank, int buf, int64_t bytes) { return static_cast<char*>(g->peer[rank][buf]) + bytes; }
+
+// tell every other member of my group: flag `kind` from me is now `seq`
+void signal_group(int kind, uint32_t seq, cudaStream_t s) {
+  uint32_t* f[kMaxSignalTargets];
+  int n = 0;
+  for (int jj = 0; jj < g->G; ++jj)
+    if (jj != g->j) f[n++] = flag_at(rank_of(g->k, jj), kind, g->rank);
+  signal_peers(f, n, seq, s);
+}
+void wait_group_peers(int kind, uint32_t seq, cudaStream_t s) {
+  for (int jj = 0; jj < g->G; ++jj)
+    if (jj != g->j) wait_flag(my_flag(kind, rank_of(g->k, jj)), seq, s);
+}
+
+int weight_pbuf(const Unit& u, int slot) {
+  return u.cls == U_E ? PB_EBUF : u.cls == U_F ? PB_FBUF : (slot ? PB_WBUF1 : PB_WBUF0);
+}
+
+void copy_stripe(void* dst, const void* src, int64_t bytes, cudaStream_t s) {
+  Timed t(s, 5, static_cast<double>(bytes));
+  TP_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice, s));
+}
+
+void gather_p2p(int uid, int slot) {
+  Ctx& c = *g;
+  const Unit& u = c.units[uid];
+  cudaStream_t s = c.ws;
+  const uint32_t seq = ++c.wseq;
+  const int64_t sb = u.s * static_cast<int64_t>(c.esz);   // stripe bytes
+  char* dst = static_cast<char*>(unit_buffer(uid, slot));
+  const int pb = weight_pbuf(u, slot);
+  if (u.cls == U_BLOCK) {
+    // WAR: if the members pulled the previous layer of this slot from my rail stripe, they must be done with it
+    if (c.wprev[slot]) wait_group_peers(SK_WDONE, c.wprev[slot], s);
+    c.wprev[slot] = (!u.owned && c.G > 1) ? seq : 0;
+  }
+  if (!u.owned) {   // rail: stripe j from the owner group's member j
+    const int src = rank_of(u.owner, c.j);
+    copy_stripe(dst + c.j * sb, peer_ptr(src, PB_WIRE, c.gofs[static_cast<size_t>(u.owner) * (c.L + 2) + uid] * c.esz),
+                sb, s);
+    if (emu_rail_crosses()) {
+      Timed t(s, 5, 0);
+      emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
+    }
+    if (c.G > 1) signal_group(SK_RAIL, seq, s);
+  } else if (c.G > 1) {   // my own stripe into the full-layer buffer
+    copy_stripe(dst + c.j * sb, wptr(c.wire, u.off), sb, s);
+  }
+  for (int jj = 0; jj < c.G; ++jj) {   // intra-group: the other stripes from the members
+    if (jj == c.j) continue;
+    const int src = rank_of(c.k, jj);
+    if (u.owned) {
+      copy_stripe(dst + jj * sb, peer_ptr(src, PB_WIRE, u.off * static_cast<int64_t>(c.esz)), sb, s);
+    } else {
+      wait_flag(my_flag(SK_RAIL, src), seq, s);
+      copy_stripe(dst + jj * sb, peer_ptr(src, pb, jj * sb), sb, s);
+    }
+  }
+  if (c.G > 1 && emu_group_crosses()) {
+    Timed t(s, 5, 0);
+    emu_delay(static_cast<double>(c.G - 1) * u.s * c.esz, s);
+  }
+  if (c.G > 1 && !u.owned && u.cls == U_BLOCK) signal_group(SK_WDONE, seq, s);
+  c.nvl_w_bytes += static_cast<double>(u.owned ? c.G - 1 : c.G) * sb;
+  ledger_gather(u, c.G, c.D, c.ledger);
+}
+
+void reduce_p2p(int uid, int slot, float* gacc) {
+  Ctx& c = *g;
+  const Unit& u = c.units[uid];
+  cudaStream_t s = c.gs;
+  const uint32_t seq = ++c.gseq;
+  const int gb = u.cls == U_E ? PB_GACCE : u.cls == U_F ? PB_GACCF : (slot ? PB_GACC1 : PB_GACC0);
+  const int ps = u.cls == U_E ? 2 : u.cls == U_F ? 3 : slot;          // rail partial slot
+  const int64_t stripe_b = static_cast<int64_t>(c.j) * u.s * 4;      // my stripe inside an fp32 accumulator
+  const int64_t part_b = static_cast<int64_t>(ps) * c.max_s * c.esz;
+  if (u.cls == U_BLOCK) c.gprev[slot] = seq;
+  if (c.G > 1) {
+    signal_group(SK_GREADY, seq, s);   // my accumulator for this unit is complete
+    wait_group_peers(SK_GREADY, seq, s);
+  }
+  if (u.owned) {
+    GradSources src;
+    int n = 0;
+    for (int kk = 0; kk < c.D; ++kk) {   // ascending group order (R16)
+      if (kk == c.k) {
+        for (int jj = 0; jj < c.G; ++jj) {   // member order
+          src.p[n] = peer_ptr(rank_of(c.k, jj), gb, stripe_b);
+          src.f32_mask |= 1u << n;
+          ++n;
+        }
+      } else {
+        wait_flag(my_flag(SK_PREADY, rank_of(kk, c.j)), seq, s);
+        src.p[n++] = peer_ptr(rank_of(kk, c.j), PB_PART, part_b);
+      }
+      src.group_end[src.n_groups++] = n;
+    }
+    if (emu_rail_crosses()) {
+      Timed t(s, 6, 0);
+      emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
+    }
+    if (emu_group_crosses()) {
+      Timed t(s, 6, 0);
+      emu_delay(static_cast<double>(c.G - 1) * u.s * 4, s);
+    }
+    adam_apply(u, src, n);
+    c.nvl_g_bytes += (4.0 * (c.G - 1) + static_cast<double>(c.esz) * (c.D - 1)) * u.s;
+    if (c.G > 1) signal_group(SK_GDONE, seq, s);
+    uint32_t* f[kMaxSignalTargets];
+    int nf = 0;
+    for (int kk = 0; kk < c.D; ++kk)
+      if (kk != c.k) f[nf++] = flag_at(rank_of(kk, c.j), SK_PDONE, c.rank);
+    signal_peers(f, nf, seq, s);
+  } else {
+    const int owner = rank_of(u.owner, c.j);
+    if (c.pprev[ps]) wait_flag(my_flag(SK_PDONE, owner), c.pprev[ps], s);   // the owner read my last partial here
+    c.pprev[ps] = seq;
+    PartialSources src;
+    for (int jj = 0; jj < c.G; ++jj) src.p[src.n++] = reinterpret_cast<const float*>(peer_ptr(rank_of(c.k, jj), gb, stripe_b));
+    {
+      Timed t(s, 6, (4.0 * c.G + c.esz) * u.s);
+      BY_TYPE(group_partial<float>(src, reinterpret_cast<float*>(static_cast<char*>(c.part) + part_b), u.s, s),
+              group_partial<bf16>(src, reinterpret_cast<bf16*>(static_cast<char*>(c.part) + part_b), u.s, s));
+      if (emu_group_crosses()) emu_delay(static_cast<double>(c.G - 1) * u.s * 4, s);
+    }
+    c.nvl_g_bytes += 4.0 * (c.G - 1) * u.s;
+    uint32_t* f = flag_at(owner, SK_PREADY, c.rank);
+    signal_peers(&f, 1, seq, s);
+    if (c.G > 1) signal_group(SK_GDONE, seq, s);
+  }
+  ledger_reduce(u, c.G, c.D, c.ledger);
 }
 
 void wait_on(cudaStream_t s, cudaEvent_t e) {
@@ -865,6 +1042,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   std::memset(c.ledger, 0, sizeof(c.ledger));
   c.regions.clear();
   c.recompute_gflop = 0;
+  c.nvl_w_bytes = c.nvl_g_bytes = 0;
   c.ev_used = 0;
   c.launches_at_start = g_kstats.launches;
   const int64_t seqs = static_cast<int64_t>(c.m) * c.Bm;
@@ -897,7 +1075,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
 
   // ---- E: gather (forward only), embed (a4)
   void* Ebuf = unit_buffer(E, 0);
-  gather(E, Ebuf);
+  gather(E, 0);
   TP_CUDA(cudaEventRecord(c.evE, c.ws));
   wait_on(c.cs, c.evE);
   for (int mb = 0; mb < c.m; ++mb) {
@@ -908,17 +1086,17 @@ double run_step(const int32_t* tokens, bool device_tokens) {
                             (bf16*)ck(0, mb), c.cs));
   }
   // ---- forward with CCO prefetch (a3, a5)
-  gather(0, unit_buffer(0, 0));
+  gather(0, 0);
   TP_CUDA(cudaEventRecord(c.w_ready[0], c.ws));
   for (int l = 0; l < c.L; ++l) {
     const int slot = l & 1;
     if (cco && l + 1 < c.L) {
       TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[(l + 1) & 1], 0));
-      gather(l + 1, unit_buffer(l + 1, (l + 1) & 1));
+      gather(l + 1, (l + 1) & 1);
       TP_CUDA(cudaEventRecord(c.w_ready[(l + 1) & 1], c.ws));
     }
     if (l == c.L - 1) {  // F lives in its own buffer: prefetch it during the last layer
-      gather(F, unit_buffer(F, 0));
+      gather(F, 0);
       TP_CUDA(cudaEventRecord(c.evF, c.ws));
     }
     wait_on(c.cs, c.w_ready[slot]);
@@ -928,7 +1106,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
     TP_CUDA(cudaEventRecord(c.w_free[slot], c.cs));
     if (!cco && l + 1 < c.L) {  // ablation: transfer serialised after the compute of the current step
       TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[slot], 0));
-      gather(l + 1, unit_buffer(l + 1, (l + 1) & 1));
+      gather(l + 1, (l + 1) & 1);
       TP_CUDA(cudaEventRecord(c.w_ready[(l + 1) & 1], c.ws));
     }
   }
@@ -939,17 +1117,18 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   for (int mb = 0; mb < c.m; ++mb) head(mb, Fbuf, c.gaccF);
   TP_CUDA(cudaEventRecord(c.evGF, c.cs));
   wait_on(c.gs, c.evGF);
-  reduce_and_update(F, c.gaccF);
+  reduce_and_update(F, 0, c.gaccF);
   // ---- backward (a7) with prefetch of l-1, gradient reduction + AdamW on gs (a8, a9)
   for (int l = c.L - 1; l >= 0; --l) {
     const int slot = l & 1;
     if (cco && l - 1 >= 0) {
       TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[(l - 1) & 1], 0));
-      gather(l - 1, unit_buffer(l - 1, (l - 1) & 1));
+      gather(l - 1, (l - 1) & 1);
       TP_CUDA(cudaEventRecord(c.w_ready[(l - 1) & 1], c.ws));
     }
     if (l != c.L - 1) wait_on(c.cs, c.w_ready[slot]);  // r = 1: layer L-1 reuses its forward buffer (R12)
     wait_on(c.cs, c.g_free[slot]);
+    if (c.p2p && c.gprev[slot]) wait_group_peers(SK_GDONE, c.gprev[slot], c.cs);   // peers done reading it
     TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.units[l].n_pad * 4, c.cs));
     void* W = unit_buffer(l, slot);
     TRACE("backward layer %d\n", l);
@@ -958,11 +1137,11 @@ double run_step(const int32_t* tokens, bool device_tokens) {
     TP_CUDA(cudaEventRecord(c.g_ready[slot], c.cs));
     if (!cco && l - 1 >= 0) {
       TP_CUDA(cudaStreamWaitEvent(c.ws, c.w_free[slot], 0));
-      gather(l - 1, unit_buffer(l - 1, (l - 1) & 1));
+      gather(l - 1, (l - 1) & 1);
       TP_CUDA(cudaEventRecord(c.w_ready[(l - 1) & 1], c.ws));
     }
     TP_CUDA(cudaStreamWaitEvent(c.gs, c.g_ready[slot], 0));
-    reduce_and_update(l, c.gacc[slot]);
+    reduce_and_update(l, slot, c.gacc[slot]);
     TP_CUDA(cudaEventRecord(c.g_free[slot], c.gs));
   }
   // ---- E backward: scatter-add into the fp32 accumulator, then reduce + update (a4, a8, a9)
@@ -974,14 +1153,16 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   }
   TP_CUDA(cudaEventRecord(c.evGE, c.cs));
   TP_CUDA(cudaStreamWaitEvent(c.gs, c.evGE, 0));
-  reduce_and_update(E, c.gaccE);
-  // ---- a10: loss
-  if (c.world > 1) TP_NCCL(ncclAllReduce(c.d_loss, c.d_loss, 1, ncclFloat64, ncclSum, c.world_comm, c.cs));
-  TP_CUDA(cudaMemcpyAsync(c.h_loss, c.d_loss, sizeof(double), cudaMemcpyDeviceToHost, c.cs));
+  reduce_and_update(E, 0, c.gaccE);
+  // ---- a10: loss.  The all-reduce runs after this rank's weight and gradient streams joined the compute stream,
+  // so its completion on any rank implies every rank finished every AdamW of the step: it is also the step
+  // barrier that orders this step's owner updates before the next step's peer pulls of the wire copies.
   TP_CUDA(cudaEventRecord(c.ev_ws1, c.ws));
   TP_CUDA(cudaEventRecord(c.ev_gs1, c.gs));
   TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_ws1, 0));
   TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_gs1, 0));
+  if (c.world > 1) TP_NCCL(ncclAllReduce(c.d_loss, c.d_loss, 1, ncclFloat64, ncclSum, c.world_comm, c.cs));
+  TP_CUDA(cudaMemcpyAsync(c.h_loss, c.d_loss, sizeof(double), cudaMemcpyDeviceToHost, c.cs));
   TP_CUDA(cudaEventRecord(c.ev_s1, c.cs));
   TP_CUDA(cudaStreamSynchronize(c.cs));
   TP_CUDA(cudaDeviceSynchronize());
@@ -1009,6 +1190,9 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   c.stats[12] = static_cast<double>(c.bytes_alloc) * 1e-9;
   c.stats[13] = static_cast<double>(c.esz);
   c.stats[15] = c.recompute_gflop;
+  c.stats[16] = c.p2p ? 1.0 : 0.0;
+  c.stats[17] = c.nvl_w_bytes * 1e-9;
+  c.stats[18] = c.nvl_g_bytes * 1e-9;
   if (c.timing) build_trace_json(ms);
   return *c.h_loss / (static_cast<double>(c.N) * c.Bm * c.S);
 }
@@ -1112,6 +1296,37 @@ Plan make_plan(int P, int G, int L, int64_t H, int64_t I, int64_t V, int rank, b
   return pl;
 }
 
+// Map every rank's weight / gradient buffers (COLLECTIVE); on success the step uses the peer path
+void setup_p2p() {
+  Ctx& c = *g;
+  const char* e = std::getenv("TAWPIPE_COMM");
+  if (c.world == 1 || c.ring || c.literal || (e && std::string(e) == "nccl")) return;
+  TP_CHECK(c.P <= kSigRanks && c.G <= kMaxPartialSources && c.G - 1 + c.D - 1 <= kMaxSignalTargets && c.G * 1 + c.D <= 16,
+           TAWPIPE_ECONFIG, "peer path: at most 64 ranks, 8 members per group, 16 gradient sources");
+  c.sig = static_cast<uint32_t*>(dmalloc(SK_N * kSigRanks * sizeof(uint32_t)));
+  TP_CUDA(cudaMemsetAsync(c.sig, 0, SK_N * kSigRanks * sizeof(uint32_t), c.cs));
+  if (c.D > 1) c.part = dmalloc(4 * c.max_s * c.esz);
+  std::vector<void*> local(PB_N, nullptr);
+  local[PB_WIRE] = c.wire;
+  local[PB_WBUF0] = c.wbuf[0];
+  local[PB_WBUF1] = c.wbuf[1];
+  local[PB_EBUF] = c.ebuf;
+  local[PB_FBUF] = c.fbuf;
+  local[PB_GACC0] = c.gacc[0];
+  local[PB_GACC1] = c.gacc[1];
+  local[PB_GACCE] = c.gaccE;
+  local[PB_GACCF] = c.gaccF;
+  local[PB_PART] = c.part;
+  local[PB_SIG] = c.sig;
+  TP_CUDA(cudaStreamSynchronize(c.cs));
+  c.p2p = peer_open(c.world_comm, c.rank, c.world, local, c.peer, c.cs);
+  c.gofs.assign(static_cast<size_t>(c.D) * (c.L + 2), 0);
+  for (int kk = 0; kk < c.D; ++kk) {
+    Plan pl = make_plan(c.P, c.G, c.L, c.H, c.I, c.V, kk * c.G, false);
+    for (int uid = 0; uid < c.L + 2; ++uid) c.gofs[static_cast<size_t>(kk) * (c.L + 2) + uid] = pl.units[uid].off;
+  }
+}
+
 void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   Ctx& c = *g;
   validate(P, G, L, d, N, c.world);
@@ -1189,6 +1404,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   if (G > 1 || D > 1) c.gwire = dmalloc(c.max_pad * esz);
   if (G > 1) c.rsout = dmalloc(c.max_s * esz);
   if (D > 1) c.crecv = dmalloc(c.max_s * (D - 1) * esz);
+  setup_p2p();   // NVLink peer mappings (GWPS on one box); NCCL collectives otherwise
   // ---- activations
   const int64_t T = c.T;
   const int m = c.m;
@@ -1319,6 +1535,7 @@ void load(const float* full, int64_t n) {
 void destroy() {
   if (!g) return;
   cudaDeviceSynchronize();
+  if (!g->peer.empty()) peer_close(g->peer, g->rank);
   for (void* p : g->allocs) cudaFree(p);
   if (g->h_tok) cudaFreeHost(g->h_tok);
   if (g->h_loss) cudaFreeHost(g->h_loss);

@@ -20,11 +20,12 @@ LIB_PATH = os.path.join(HERE, "libtawpipe.so")
 OK, ECONFIG, EINVARIANT, ERUNTIME, EUNINIT = 0, -2, -3, -4, -5
 FP32, BF16 = 0, 1
 GWPS, NO_CCO, RING, LITERAL = 0, 1, 2, 4
-LEDGER_N, STATS_N = 24, 16
+LEDGER_N, STATS_N = 24, 19
 
 STATS_NAMES = ("step_ms", "exposed_comm_ms", "weight_comm_ms", "grad_comm_ms", "gemm_ms", "gemm_gflop",
                "gemm_launches", "attn_ms", "attn_gflop", "adamw_ms", "adamw_gb", "kernel_launches",
-               "alloc_gb", "wire_bytes", "elementwise_ms", "recompute_gflop")
+               "alloc_gb", "wire_bytes", "elementwise_ms", "recompute_gflop", "p2p", "nvlink_weight_gb",
+               "nvlink_grad_gb")
 
 
 class TawpipeError(RuntimeError):

@@ -44,7 +44,7 @@ def main():
     sess.load(T.pack_full_model(params))
     if a.emu_gbps > 0:
         sess.set_link_emulation(a.emu_gbps, 30.0, a.emu_node)
-        sess.set_timing(True)
+    sess.set_timing(True)
     losses, ledgers, comm_ms = [], [], []
     for step in range(a.steps):
         toks = synth.tokens(a.N, cfg.micro_bs, cfg.seq, cfg.vocab, step=step)
@@ -53,7 +53,7 @@ def main():
         stt = sess.stats()
         comm_ms.append(stt["weight_comm_ms"] + stt["grad_comm_ms"])
     np.savez(os.path.join(a.out, f"rank{rank}.npz"), losses=np.array(losses), ledgers=np.array(ledgers, np.uint64),
-             shard=sess.shard(), comm_ms=np.array(comm_ms))
+             shard=sess.shard(), comm_ms=np.array(comm_ms), p2p=np.array(stt["p2p"]))
     sess.close()
 
 

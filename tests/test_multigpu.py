@@ -44,6 +44,13 @@ CASES = [
 CASES = [c if len(c) == 12 else c + (0.0, 0) for c in CASES]
 # every case runs AdamW in its linear regime (ε = 1 ≫ |g|, lr = 1, no decay: Δ ≈ −m̂, R18) so that e_Δ sees a wrong
 # gradient scale (a double-counted or missing group partial); two cases keep the default ε = 1e-8 (e_θ only)
+# GWPS runs the NVLink peer path by default (IPC copies + in-kernel gradient reads); "-nccl" cases force the NCCL
+# collectives (TAWPIPE_COMM=nccl) so both implementations of a3/a8/a9 stay covered
+CASES += [("c0-2x2-nccl", C0, 4, 2, 2, 4, 0, 0, False, False, 0.0, 0),
+          ("c0b-2x2-bf16-nccl", C0B, 4, 2, 2, 4, 1, 1, False, False, 0.0, 0),
+          ("c0-2x2-g2x-p2p-bf16-ckpt2", C0B, 4, 2, 4, 8, 1, 2, False, False, 0.0, 0),
+          ("c0-1x2-fsdp-bf16", C0B, 2, 2, 2, 4, 1, 0, False, False, 0.0, 0),
+          ("c0-2x1-bf16", C0B, 2, 1, 2, 2, 1, 0, False, False, 0.0, 0)]
 CASES = [c + (True,) for c in CASES] + [("c0-2x2-default-eps", C0, 4, 2, 2, 4, 0, 0, False, False, 0.0, 0, False),
                                        ("c0b-1x2-bf16-default-eps", C0B, 2, 2, 2, 2, 1, 0, False, False, 0.0, 0,
                                         False)]
@@ -72,13 +79,17 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
            "--dtype", str(dtype), "--ckpt", str(ckpt), "--out", str(tmp_path)] + (["--no-cco"] if no_cco else []) \
         + (["--ring"] if ring else []) + (["--literal"] if literal else []) + (["--linear"] if linear else []) \
         + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
+    env = dict(os.environ, TAWPIPE_COMM="nccl") if name.endswith("-nccl") else dict(os.environ)
     for _ in range(3):   # the free port can be taken between probing and torchrun's bind: retry on EADDRINUSE
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
         if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
             break
         cmd[cmd.index(next(c for c in cmd if c.startswith("--master-port=")))] = f"--master-port={free_port()}"
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
+    # which implementation ran: the peer path for GWPS unless forced to NCCL; ring / literal always NCCL
+    want_p2p = not (ring or literal or name.endswith("-nccl"))
+    assert all(bool(x["p2p"]) == want_p2p for x in res), [float(x["p2p"]) for x in res]
     # oracle: plain single-device step on the same tokens
     params = synth.perturb_gains(synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab))
     st = om.init_state(params)

@@ -18,6 +18,15 @@ C0 = dict(n_layers=2, hidden=64, heads=4, ffn=192, vocab=256, seq=128, micro_bs=
 C0B = dict(n_layers=2, hidden=256, heads=2, ffn=768, vocab=512, seq=256, micro_bs=1)
 
 
+# e_Δ bar in the linear AdamW regime (ε = 1 ≫ |g|, lr = 1, no decay; R18 in DESIGN.md): there Δ ≈ −m̂ ∝ g, so e_Δ is
+# the gradient error relative to the tensor's largest gradient element.  fp32: the fp32 sums over all tokens of a
+# step (dγ of RMSNorm, the wgrad reductions) cancel to ~1e-3 of their terms' scale and leave up to ~1e-4 of max|g|
+# (measured 1.6e-4 on layers.0.mlp_norm at C0); bf16: one bf16 rounding of every activation / weight on the path.
+# Both bars sit far below what a structural error produces: a dropped or doubled group / micro-batch contribution
+# moves Δ by ≥ 1/(number of contributions) ≥ 1/16 here, a 2× scale error by 1.
+TOL_DELTA = {0: 1e-3, 1: 5e-2}
+
+
 def oracle_cfg(d, **kw):
     x = dict(d)
     x.update(kw)

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import synth
-from helpers import C0, C0B, om, oracle_cfg, reassemble, weight_errors
+from helpers import C0, C0B, TOL_DELTA, om, oracle_cfg, reassemble, weight_errors
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -66,7 +66,8 @@ def run_parity(T, base, dtype, tol_loss, tol_w, kappa, ckpt=0, n_micro=4, steps=
                       f"off-W {off:.3%} violations {viol}")
                 # e_Δ: every step in the linear cases; otherwise the step-1 check (Δ = −lr(wd·θ + g/(|g|+ε)) is
                 # well conditioned there; later AdamW's m/√v cancellation amplifies rounding, R18 reading)
-                assert et <= tol_w and ((step > 0 and not linear) or ed <= tol_w) and viol == 0, (
+                tol_d = TOL_DELTA[dtype] if linear else tol_w
+                assert et <= tol_w and ((step > 0 and not linear) or ed <= tol_d) and viol == 0, (
                     step, et, ed, viol, sorted(rep, key=lambda r: -max(r[1], r[2]))[:3])
         led = sess.ledger()
         assert all(x == 0 for x in led)   # P = 1: no communication at all

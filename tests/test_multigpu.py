@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import synth
-from helpers import C0, C0B, ROOT, om, oracle_cfg, reassemble, weight_errors
+from helpers import C0, C0B, ROOT, TOL_DELTA, om, oracle_cfg, reassemble, weight_errors
 from oracle import layout as OL
 from oracle import ledger as LG
 
@@ -81,7 +81,7 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
         + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
     env = dict(os.environ, TAWPIPE_COMM="nccl") if name.endswith("-nccl") else dict(os.environ)
     for _ in range(3):   # the free port can be taken between probing and torchrun's bind: retry on EADDRINUSE
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
         if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
             break
         cmd[cmd.index(next(c for c in cmd if c.startswith("--master-port=")))] = f"--master-port={free_port()}"
@@ -96,6 +96,7 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
     theta0 = om.to_f64(params)
     grads = []
     tol_loss, tol_w, kappa = (1e-5, 1e-4, 1e-3) if dtype == 0 else (1e-2, 2e-2, 5e-2)
+    tol_d = TOL_DELTA[dtype]
     for step in range(steps):
         toks = synth.tokens(N, cfg.micro_bs, cfg.seq, cfg.vocab, step=step)
         lr, g = om.train_step(st, toks, cfg)
@@ -107,7 +108,7 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
     gpu = reassemble(cfg, P, G, [x["shard"] for x in res], literal=literal)
     et, ed, viol, off, rep = weight_errors(gpu, st.params, theta0, grads, cfg, kappa)
     print(f"{name}: e_theta {et:.2e} e_delta {ed:.2e} off-W {off:.3%} violations {viol}")
-    assert et <= tol_w and viol == 0 and (ed <= tol_w or not linear), (
+    assert et <= tol_w and viol == 0 and (ed <= tol_d or not linear), (
         et, ed, viol, sorted(rep, key=lambda z: -max(z[1], z[2]))[:3])
     # byte ledger: bit-exact against the closed forms, every rank, every step
     H, V = cfg.hidden, cfg.vocab

@@ -142,6 +142,7 @@ struct Ctx {
   void* part = nullptr;                   // rail partials of this rank's group (4 slots: layer 0/1, E, F) × max_s
   uint32_t wseq = 0, gseq = 0;            // gathers / reductions issued so far (identical on every rank)
   uint32_t wprev[2] = {0, 0}, gprev[2] = {0, 0}, pprev[4] = {0, 0, 0, 0};
+  int pprev_owner[4] = {0, 0, 0, 0};      // the rank that read the previous partial in that slot
   double nvl_w_bytes = 0, nvl_g_bytes = 0;   // bytes this rank pulled / read over NVLink in the last step
   // events
   cudaEvent_t w_ready[2], w_free[2], g_ready[2], g_free[2], evE, evF, evGF, evGE, ev_s0, ev_s1, ev_ws0, ev_ws1,
@@ -709,8 +710,12 @@ void gather_p2p(int uid, int slot) {
       emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
     }
     if (c.G > 1) signal_group(SK_RAIL, seq, s);
-  } else if (c.G > 1) {   // my own stripe into the full-layer buffer
-    copy_stripe(dst + c.j * sb, wptr(c.wire, u.off), sb, s);
+  } else {
+    if (c.G > 1) copy_stripe(dst + c.j * sb, wptr(c.wire, u.off), sb, s);   // my own stripe into the layer buffer
+    if (emu_rail_crosses()) {   // emulated link: the owner's link carries its stripe to the D − 1 other groups
+      Timed t(s, 5, 0);
+      emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
+    }
   }
   for (int jj = 0; jj < c.G; ++jj) {   // intra-group: the other stripes from the members
     if (jj == c.j) continue;
@@ -779,8 +784,10 @@ void reduce_p2p(int uid, int slot, float* gacc) {
     signal_peers(f, nf, seq, s);
   } else {
     const int owner = rank_of(u.owner, c.j);
-    if (c.pprev[ps]) wait_flag(my_flag(SK_PDONE, owner), c.pprev[ps], s);   // the owner read my last partial here
+    // WAR: the owner that read the previous partial in this slot (layers alternate owners) is done with it
+    if (c.pprev[ps]) wait_flag(my_flag(SK_PDONE, c.pprev_owner[ps]), c.pprev[ps], s);
     c.pprev[ps] = seq;
+    c.pprev_owner[ps] = owner;
     PartialSources src;
     for (int jj = 0; jj < c.G; ++jj) src.p[src.n++] = reinterpret_cast<const float*>(peer_ptr(rank_of(c.k, jj), gb, stripe_b));
     {
@@ -788,6 +795,8 @@ void reduce_p2p(int uid, int slot, float* gacc) {
       BY_TYPE(group_partial<float>(src, reinterpret_cast<float*>(static_cast<char*>(c.part) + part_b), u.s, s),
               group_partial<bf16>(src, reinterpret_cast<bf16*>(static_cast<char*>(c.part) + part_b), u.s, s));
       if (emu_group_crosses()) emu_delay(static_cast<double>(c.G - 1) * u.s * 4, s);
+      // emulated link: the rail exchange that delivers this partial to the owner (as on the NCCL path)
+      if (emu_rail_crosses()) emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
     }
     c.nvl_g_bytes += 4.0 * (c.G - 1) * u.s;
     uint32_t* f = flag_at(owner, SK_PREADY, c.rank);

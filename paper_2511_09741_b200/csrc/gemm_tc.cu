@@ -19,7 +19,11 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <mutex>
+#include <set>
+#include <string>
+#include <utility>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -174,11 +178,34 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int64_t row, int n
   }
 }
 
+// Grouped rasterisation of the persistent tile loop (t = linear tile index):
+//   raster > 0: bands of `raster` M-tiles sweep over all N-tiles (the A band stays in L2, B streams once per band);
+//   raster < 0: bands of −raster N-tiles sweep over all M-tiles (the B band stays in L2, A streams once per band).
+// The host picks the orientation and band size that minimise the HBM reads of the operands (choose_raster).
+__device__ __forceinline__ void grouped_tile(int t, int num_m, int num_n, int raster, int& mb, int& nb) {
+  if (raster > 0) {
+    const int group_size = raster * num_n;
+    const int first_m = (t / group_size) * raster;
+    const int gm = min(raster, num_m - first_m);
+    const int r = t % group_size;
+    mb = first_m + r % gm;
+    nb = r / gm;
+  } else {
+    const int G = -raster;
+    const int group_size = G * num_m;
+    const int first_n = (t / group_size) * G;
+    const int gn = min(G, num_n - first_n);
+    const int r = t % group_size;
+    nb = first_n + r % gn;
+    mb = r / gn;
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
                    int64_t ldc, const bf16* __restrict__ R, int M, int N, int K, void* __restrict__ aux, int64_t ldx,
-                   int64_t I) {
+                   int64_t I, int raster) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -212,17 +239,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // grouped rasterisation: 16 M-tiles share each sweep over N for L2 reuse
-  auto tile_coords = [&](int t, int& mb, int& nb) {
-    constexpr int GROUP = 16;
-    const int group_size = GROUP * num_n;
-    const int g = t / group_size;
-    const int first_m = g * GROUP;
-    const int gm = min(GROUP, num_m - first_m);
-    const int r = t % group_size;
-    mb = first_m + r % gm;
-    nb = r / gm;
-  };
+  auto tile_coords = [&](int t, int& mb, int& nb) { grouped_tile(t, num_m, num_n, raster, mb, nb); };
 
   if (warp == 4) {
     if (lane == 0) {
@@ -342,7 +359,7 @@ template <bool A_MN, bool B_MN, int EPI, int NSTAGE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     void* __restrict__ C, int64_t ldc, const bf16* __restrict__ R, int M, int N, int K,
-                    void* __restrict__ aux, int64_t ldx, int64_t I) {
+                    void* __restrict__ aux, int64_t ldx, int64_t I, int raster) {
   using Cfg = Gemm2Cfg<NSTAGE>;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -379,16 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto tile_coords = [&](int t, int& mb, int& nb) {
-    constexpr int GROUP = 8;   // 8 pair tiles = 2048 rows share each sweep over N
-    const int group_size = GROUP * num_n;
-    const int g = t / group_size;
-    const int first_m = g * GROUP;
-    const int gm = min(GROUP, num_m - first_m);
-    const int r = t % group_size;
-    mb = first_m + r % gm;
-    nb = r / gm;
-  };
+  auto tile_coords = [&](int t, int& mb, int& nb) { grouped_tile(t, num_m, num_n, raster, mb, nb); };
 
   if (warp == 4) {
     if (lane == 0) {
@@ -541,15 +549,46 @@ namespace {
 
 int g_num_sms = 0;
 
+// L2-aware raster: keep a band of one operand resident (≤ kL2Band bytes) and stream the other once per band; pick
+// the orientation with the fewer estimated HBM operand reads.  Long-K GEMMs (the wgrads, K = tokens) stream K in
+// lockstep across the in-flight tiles, so their reuse is per K slice and the default M-band order is kept.
+// TAWPIPE_GEMM_RASTER=m|n|default forces an orientation (experiments).
+int choose_raster(int64_t num_m, int64_t num_n, int64_t rows_m, int64_t rows_n, int64_t K, int default_group) {
+  static const int force = [] {
+    const char* e = std::getenv("TAWPIPE_GEMM_RASTER");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "m" ? 1 : v == "n" ? 2 : v == "default" ? 3 : 0;
+  }();
+  constexpr int64_t kL2Band = 48ll << 20, kLongK = 8ll << 20;
+  const int64_t bm = rows_m * K * 2, bn = rows_n * K * 2;   // bytes of one M-tile band / one N-tile band
+  if (force == 3 || (force == 0 && bm > kLongK && bn > kLongK)) return default_group;
+  const int64_t gm = std::max<int64_t>(1, std::min<int64_t>(num_m, kL2Band / bm));
+  const int64_t gn = std::max<int64_t>(1, std::min<int64_t>(num_n, kL2Band / bn));
+  const int64_t a_bytes = num_m * bm, b_bytes = num_n * bn;
+  const int64_t reads_m = a_bytes + b_bytes * ((num_m + gm - 1) / gm);
+  const int64_t reads_n = b_bytes + a_bytes * ((num_n + gn - 1) / gn);
+  const bool use_n = force == 2 || (force == 0 && reads_n < reads_m);
+  return use_n ? -static_cast<int>(gn) : static_cast<int>(gm);
+}
+
+// the dynamic shared-memory limit is a per-device attribute: set it once per (kernel, device)
+template <typename K>
+void set_smem_attr(K kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  TP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert({reinterpret_cast<const void*>(kern), dev}).second)
+    TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch(const GemmArgs& g, cudaStream_t s) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    attr_set = true;
-  }
+  set_smem_attr(kern, Cfg::SMEM);
   if (g_num_sms == 0) {
     int dev;
     TP_CUDA(cudaGetDevice(&dev));
@@ -561,8 +600,9 @@ void launch(const GemmArgs& g, cudaStream_t s) {
                         : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, EPI == EPI_SWIGLU_FWD ? BN / 2 : BN);
   const int tiles = static_cast<int>((g.M / BM) * (g.N / BN));
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int raster = choose_raster(g.M / BM, g.N / BN, BM, BN, g.K, 16);
   kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
-                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I);
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }
@@ -600,8 +640,8 @@ void launch2_n(const GemmArgs& g, cudaStream_t s) {
   auto kern = gemm_tc2_kernel<A_MN, B_MN, EPI, NSTAGE>;
   static bool attr_set = false;
   static int max_clusters = 0;
+  set_smem_attr(kern, Cfg::SMEM);
   if (!attr_set) {
-    TP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * 148);
     cfg.blockDim = dim3(192);
@@ -622,8 +662,9 @@ void launch2_n(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap tb = B_MN ? make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 64) : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, Cfg::BN / 2);
   const int tiles = static_cast<int>((g.M / (2 * BM)) * (g.N / Cfg::BN));
   const int grid = 2 * (tiles < clusters_fit ? tiles : clusters_fit);
+  const int raster = choose_raster(g.M / (2 * BM), g.N / Cfg::BN, 2 * BM, Cfg::BN, g.K, 8);
   kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
-                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I);
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }

@@ -52,7 +52,10 @@ CASES += [("c0-2x2-nccl", C0, 4, 2, 2, 4, 0, 0, False, False, 0.0, 0),
           ("c0-1x2-fsdp-bf16", C0B, 2, 2, 2, 4, 1, 0, False, False, 0.0, 0),
           ("c0-2x1-bf16", C0B, 2, 1, 2, 2, 1, 0, False, False, 0.0, 0),
           # D = 4 groups of 1 with 8 layers: consecutive layers sharing a buffer slot have different owners
-          ("c0b-4x1-L8-bf16", C0B, 4, 1, 8, 4, 1, 1, False, False, 0.0, 0)]
+          ("c0b-4x1-L8-bf16", C0B, 4, 1, 8, 4, 1, 1, False, False, 0.0, 0),
+          ("c0b-4x1-L8-bf16-nccl", C0B, 4, 1, 8, 4, 1, 1, False, False, 0.0, 0),
+          ("c0b-2x2-L4-bf16-nccl", C0B, 4, 2, 4, 8, 1, 2, False, False, 0.0, 0),
+          ("c0-4x1-L8-fp32", C0, 4, 1, 8, 4, 0, 1, False, False, 0.0, 0)]
 CASES = [c + (True,) for c in CASES] + [("c0-2x2-default-eps", C0, 4, 2, 2, 4, 0, 0, False, False, 0.0, 0, False),
                                        ("c0b-1x2-bf16-default-eps", C0B, 2, 2, 2, 2, 1, 0, False, False, 0.0, 0,
                                         False)]

@@ -271,8 +271,18 @@ __device__ __forceinline__ void st8f(float* p, const float (&f)[8]) {
   reinterpret_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
   reinterpret_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
 }
-__device__ __forceinline__ void ld8w(const float* p, float (&f)[8]) { ld8f(p, f); }
-__device__ __forceinline__ void ld8w(const bf16* p, float (&f)[8]);
+// gradient sources may be PEER memory (IPC mappings): read them with ld.global.cg so that no line of a peer buffer
+// is ever served from this SM's L1 -- peer addresses bypass the local L2 and only L1 caches them, and a line left
+// there by the previous layer's read of the same buffer slot was observed to survive into a later kernel
+__device__ __forceinline__ void ld8src(const float* p, float (&f)[8]) {
+  const float4 a = __ldcg(reinterpret_cast<const float4*>(p)), b = __ldcg(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+__device__ __forceinline__ void ld8src(const bf16* p, float (&f)[8]);
+__device__ __forceinline__ float ld1src(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ float ld1src(const bf16* p) {
+  return __uint_as_float(static_cast<uint32_t>(__ldcg(reinterpret_cast<const unsigned short*>(p))) << 16);
+}
 __device__ __forceinline__ void st8w(float* p, const float (&f)[8]) { st8f(p, f); }
 __device__ __forceinline__ void st8w(bf16* p, const float (&f)[8]);
 
@@ -304,9 +314,9 @@ __global__ void __launch_bounds__(256) adamw_grouped_v8_kernel(GradSources src, 
       for (int si = s0; si < src.group_end[gi]; ++si) {   // member order
         float x[8];
         if (src.f32_mask >> si & 1u)
-          ld8f(static_cast<const float*>(src.p[si]) + i, x);
+          ld8src(static_cast<const float*>(src.p[si]) + i, x);
         else
-          ld8w(static_cast<const W*>(src.p[si]) + i, x);
+          ld8src(static_cast<const W*>(src.p[si]) + i, x);
 #pragma unroll
         for (int e = 0; e < 8; ++e) part[e] += x[e];
       }
@@ -339,8 +349,8 @@ __global__ void adamw_grouped_kernel(GradSources src, float* __restrict__ master
     for (int gi = 0; gi < src.n_groups; ++gi) {
       float part = 0.f;
       for (int si = s0; si < src.group_end[gi]; ++si)
-        part += (src.f32_mask >> si & 1u) ? static_cast<const float*>(src.p[si])[i]
-                                          : to_f(static_cast<const W*>(src.p[si])[i]);
+        part += (src.f32_mask >> si & 1u) ? ld1src(static_cast<const float*>(src.p[si]) + i)
+                                          : ld1src(static_cast<const W*>(src.p[si]) + i);
       s0 = src.group_end[gi];
       tot = gi == 0 ? part : tot + part;
     }
@@ -372,7 +382,16 @@ __device__ __forceinline__ void st8(bf16* p, const float (&f)[8]) {
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = u;
 }
-__device__ __forceinline__ void ld8w(const bf16* p, float (&f)[8]) { ld8(p, f); }
+__device__ __forceinline__ void ld8src(const bf16* p, float (&f)[8]) {
+  const uint4 u = __ldcg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(h[i]);
+    f[2 * i] = x.x;
+    f[2 * i + 1] = x.y;
+  }
+}
 __device__ __forceinline__ void st8w(bf16* p, const float (&f)[8]) { st8(p, f); }
 
 // grid (rows), block = nblk·nh·(half/8) threads (<= 1024): each thread rotates 8 pairs of one head

@@ -54,9 +54,10 @@ __global__ void __launch_bounds__(256) group_partial_kernel(PartialSources src, 
   const int64_t n4 = n / 4;
   for (int64_t i4 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i4 < n4;
        i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float4 acc = reinterpret_cast<const float4*>(src.p[0])[i4];
+    // peer memory: ld.global.cg, never through this SM's L1 (see kernels.cu ld8src)
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(src.p[0]) + i4);
     for (int m = 1; m < src.n; ++m) {
-      const float4 x = reinterpret_cast<const float4*>(src.p[m])[i4];
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(src.p[m]) + i4);
       acc.x += x.x;
       acc.y += x.y;
       acc.z += x.z;

@@ -123,6 +123,7 @@ struct Ctx {
   std::vector<void*> dhb;  // m: gradient of the residual stream per micro-batch
   void *dY = nullptr, *dGU = nullptr, *db = nullptr, *dh1 = nullptr, *dO = nullptr, *dqkv = nullptr, *da = nullptr;
   float *delta = nullptr, *dq_acc = nullptr;
+  void* barrier_buf = nullptr;  // one int for world_barrier
   void* emb_scratch = nullptr;  // deterministic embedding backward: sort keys / positions + CUB temp
   size_t emb_scratch_bytes = 0;
   void *fnorm = nullptr, *logits = nullptr, *df = nullptr;
@@ -176,6 +177,16 @@ void* dmalloc(size_t bytes) {
   g->allocs.push_back(p);
   g->bytes_alloc += bytes;
   return p;
+}
+
+// Device-side barrier of all ranks (a one-int NCCL all-reduce on the compute stream, then a host wait).  The
+// peer path pulls owners' wire copies without a rendezvous, so every operation that rewrites them outside a step
+// (the device-side init in tawpipe_init, tawpipe_load) ends with this barrier.
+void world_barrier() {
+  if (g->world <= 1) return;
+  int* d = static_cast<int*>(g->barrier_buf);
+  TP_NCCL(ncclAllReduce(d, d, 1, ncclInt, ncclSum, g->world_comm, g->cs));
+  TP_CUDA(cudaStreamSynchronize(g->cs));
 }
 
 cudaEvent_t pool_event() {
@@ -1515,6 +1526,9 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
             cast_f32<bf16>(ms, (bf16*)wptr(c.wire, u.off), u.s, c.cs));
   }
   TP_CUDA(cudaStreamSynchronize(c.cs));
+  c.barrier_buf = dmalloc(sizeof(int));
+  TP_CUDA(cudaMemset(c.barrier_buf, 0, sizeof(int)));
+  world_barrier();   // every owner's wire copy is initialised before any peer can pull it
   c.inited = true;
 }
 
@@ -1538,6 +1552,7 @@ void load(const float* full, int64_t n) {
   TP_CUDA(cudaMemsetAsync(c.mom, 0, c.owned_total * 4, c.cs));
   TP_CUDA(cudaMemsetAsync(c.vel, 0, c.owned_total * 4, c.cs));
   TP_CUDA(cudaStreamSynchronize(c.cs));
+  world_barrier();   // no peer pulls a wire copy this rank is still rewriting
   c.step_t = 0;
 }
 

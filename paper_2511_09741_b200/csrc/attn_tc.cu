@@ -774,13 +774,8 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
       }
     }
   } else if (warp < 4) {
-    // The softmax-gradient passes read Sᵀ / dPᵀ with the 16-lane TMEM shapes: thread (t0 = lane % 4, t1 = lane / 4)
-    // of half hh holds key rows kA = 32·warp + 16·hh + t1 and kB = kA + 8, query columns 8r + 2·t0 (+1) for
-    // repetitions r.  A quad of lanes then covers 8 consecutive query columns, so each thread needs LSE / δ of only
-    // 32 of the 128 columns, read as conflict-free LDS.64 (the thread-per-row form read all 128 of each per thread,
-    // ≈1,000 broadcast shared-memory wavefronts per key tile -- a quarter of the kernel's smem pipe), and the dSᵀ
-    // stores stay conflict-free 128-byte wavefronts (a quad writes one 16-byte chunk of each of its rows).
-    const int t0 = lane & 3, t1 = lane >> 2;
+    const int t = warp * 32 + lane;  // key row of the tile (TMEM lane)
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     uint8_t* sDS = sm + L::OFF_DS;
     for (int it = 0; it < n_it; ++it) {
       const int st = it & 1;
@@ -788,42 +783,36 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
       const float* dl = del_s + st * 128;
       mbar_wait(&q_full[st], (it >> 1) & 1);   // LSE_i, δ_i landed (bulk copies on the same barrier as Q_i)
       mbar_wait(s_full, it & 1);
-      if (warp == 0 && lane == 0) TR(it, 4);
+      if (t == 0) TR(it, 4);
       tc_fence_after();
+#pragma unroll
       // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
-      uint32_t pk[2][2][16];   // Pᵀ_it packed bf16 [half][row A/B][rep], kept for the dS pass
+      uint32_t pk[4][16];   // Pᵀ_it, packed bf16, kept for the dS pass (Sᵀ_{it+1} overwrites its TMEM copy)
       auto p_pass = [&](auto diag) {
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t lanes = static_cast<uint32_t>(warp * 32 + hh * 16) << 16;
-          const int kA = warp * 32 + hh * 16 + t1;
+        for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+          uint32_t uu[2][32];
+          tmem_ld32(tS + lane_off + cp * 32, uu[0]);
+          tmem_ld32(tS + lane_off + cp * 32 + 32, uu[1]);
+          tmem_wait_ld();
 #pragma unroll
-          for (int cb = 0; cb < 2; ++cb) {   // 64 query columns per TMEM round trip
-            uint32_t u[32];
-            tmem_ld_16x256b_x8(tS + lanes + cb * 64, u);
-            tmem_wait_ld();
-            uint32_t pw[16];
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int c = cp + h2;
+            uint32_t (&pw)[16] = pk[c];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              const int col = cb * 64 + r * 8 + 2 * t0;
-              const float2 l2 = *reinterpret_cast<const float2*>(ls + col);
-              const float2 a2 = ffma2(make_float2(__uint_as_float(u[4 * r]), __uint_as_float(u[4 * r + 1])),
+            for (int k = 0; k < 32; k += 2) {
+              const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
+              const float2 a2 = ffma2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
                                       make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
-              const float2 b2 = ffma2(make_float2(__uint_as_float(u[4 * r + 2]), __uint_as_float(u[4 * r + 3])),
-                                      make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
-              float pa0 = ex2(a2.x), pa1 = ex2(a2.y), pb0 = ex2(b2.x), pb1 = ex2(b2.y);
+              float p0 = ex2(a2.x);
+              float p1 = ex2(a2.y);
               if (decltype(diag)::value) {  // query index < key index is masked
-                if (col < kA) pa0 = 0.f;
-                if (col + 1 < kA) pa1 = 0.f;
-                if (col < kA + 8) pb0 = 0.f;
-                if (col + 1 < kA + 8) pb1 = 0.f;
+                if (c * 32 + k < t) p0 = 0.f;
+                if (c * 32 + k + 1 < t) p1 = 0.f;
               }
-              pk[hh][0][cb * 8 + r] = pw[2 * r] = pack_bf16(pa0, pa1);
-              pk[hh][1][cb * 8 + r] = pw[2 * r + 1] = pack_bf16(pb0, pb1);
+              pw[k / 2] = pack_bf16(p0, p1);
             }
-            // packed column 4r + t0 of block cb holds P columns (8r + 2t0, +1): the packed-bf16 A operand of dV;
-            // it overwrites Sᵀ columns already read (32·cb .. 32·cb + 31 < 64·cb + 64)
-            tmem_st_16x128b_x8(tS + lanes + cb * 32, pw);
+            tmem_st16(tS + lane_off + c * 16, pw);  // overwrites Sᵀ columns already read (c*16 < cp*32+64)
           }
         }
       };
@@ -834,48 +823,46 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_ready);
-      if (warp == 0 && lane == 0) TR(it, 5);
+      if (t == 0) TR(it, 5);
       mbar_wait(dp_full, it & 1);
-      if (warp == 0 && lane == 0) TR(it, 6);
+      if (t == 0) TR(it, 6);
       if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ of the previous tile consumed by dK / dQ
-      if (warp == 0 && lane == 0) TR(it, 7);
+      if (t == 0) TR(it, 7);
       tc_fence_after();
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t lanes = static_cast<uint32_t>(warp * 32 + hh * 16) << 16;
-        const int kA = warp * 32 + hh * 16 + t1;   // kA % 8 == t1: the SW128 chunk swizzle of both rows is r ^ t1
+      for (int cp = 0; cp < 4; cp += 2) {  // two chunks per TMEM round trip
+        uint32_t uu[2][32];
+        tmem_ld32(tdP + lane_off + cp * 32, uu[0]);
+        tmem_ld32(tdP + lane_off + cp * 32 + 32, uu[1]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int cb = 0; cb < 2; ++cb) {
-          uint32_t u[32];
-          tmem_ld_16x256b_x8(tdP + lanes + cb * 64, u);
-          tmem_wait_ld();
-          uint8_t* atom = sDS + cb * ATOM;
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = cp + h2;
+          const uint32_t (&pp)[16] = pk[c];
+          uint32_t d[16];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const int col = cb * 64 + r * 8 + 2 * t0;
-            const float2 d2 = *reinterpret_cast<const float2*>(dl + col);
-            const uint32_t pa = pk[hh][0][cb * 8 + r], pb = pk[hh][1][cb * 8 + r];
-            const float2 dsa = fmul2(make_float2(bf_lo(pa), bf_hi(pa)),
-                                     fadd2(make_float2(__uint_as_float(u[4 * r]), __uint_as_float(u[4 * r + 1])),
-                                           make_float2(-d2.x, -d2.y)));
-            const float2 dsb = fmul2(make_float2(bf_lo(pb), bf_hi(pb)),
-                                     fadd2(make_float2(__uint_as_float(u[4 * r + 2]), __uint_as_float(u[4 * r + 3])),
-                                           make_float2(-d2.x, -d2.y)));
-            // dSᵀ row k, columns (col, col + 1): 4 bytes of 16-byte chunk r of atom cb, SW128-swizzled
-            const int off = ((r ^ t1) << 4) + 4 * t0;
-            *reinterpret_cast<uint32_t*>(atom + kA * 128 + off) = pack_bf16(dsa.x, dsa.y);
-            *reinterpret_cast<uint32_t*>(atom + (kA + 8) * 128 + off) = pack_bf16(dsb.x, dsb.y);
+          for (int k = 0; k < 32; k += 2) {
+            const float2 dl2 = *reinterpret_cast<const float2*>(dl + c * 32 + k);
+            const float2 ds2 = fmul2(make_float2(bf_lo(pp[k / 2]), bf_hi(pp[k / 2])),
+                                     fadd2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
+                                           make_float2(-dl2.x, -dl2.y)));
+            d[k / 2] = pack_bf16(ds2.x, ds2.y);
+          }
+          // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int chunk = (c & 1) * 4 + v;
+            *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
+                make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
           }
         }
       }
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(ds_ready);
-      if (warp == 0 && lane == 0) TR(it, 8);
+      if (t == 0) TR(it, 8);
       if (lane == 0) TR(it, 12 + warp);   // per-warp dS done
     }
-    const int t = warp * 32 + lane;  // key row of the tile (TMEM lane) for the dK / dV epilogue
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     // dK (× softmax scale) and dV rows of this key tile
     mbar_wait(mm2_done, (n_it - 1) & 1);
     tc_fence_after();

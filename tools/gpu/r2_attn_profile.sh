@@ -9,4 +9,3 @@ echo "ncu attn rc=$?"; tail -3 gpurun_out/r2_ncu_attn.log
 ncu --set full --clock-control none -k regex:"adamw|rmsnorm|ce_kernel|embed_segment" -c 8 \
     -o gpurun_out/r2_hbm python tools/hbm_kernels.py --once > gpurun_out/r2_ncu_hbm.log 2>&1
 echo "ncu hbm rc=$?"; tail -3 gpurun_out/r2_ncu_hbm.log
-python bench.py --steps 5 --warmup 3 > gpurun_out/r2_bench_n1.json 2> gpurun_out/r2_bench_n1.err; echo "bench rc=$?"; cat gpurun_out/r2_bench_n1.json | head -c 3000

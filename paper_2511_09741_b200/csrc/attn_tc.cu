@@ -941,324 +941,6 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
 }
 
 
-// ----------------------------------------------------------------------------------------------- backward v8
-// As fa_bwd (v5), with twice the softmax-gradient warps: the in-kernel timeline showed the P pass (≈1,840 cycles,
-// MUFU floor 1,024) and the dS pass (≈1,290) of one warp per SMSP on the critical chain of every key tile
-// (≈3,900 cycles per tile against 2,560 of tensor work).  Warps 0-7 now split the 128 query columns of a tile:
-// warp w handles TMEM lane quarter w % 4 and query columns 64·(w / 4) .. +63, so each SMSP runs two softmax warps.
-// Pᵀ of columns half ch is packed into TMEM columns 64·ch .. 64·ch + 31 (each warp overwrites only Sᵀ columns it
-// has already read), and the dV MMA takes its A operand from those two ranges.
-//   warps 0-7 softmax gradient, 8-11 dQ drain, 12 TMA producer, 13 / 14 MMA issuers X / Y (SMSPs 1 / 2), 15 idle.
-//   Registers are rebalanced per warpgroup with setmaxnreg: softmax 144, dQ 168, producer / issuers 56 (65,536).
-template <int DH>
-__global__ void __launch_bounds__(512, 1)
-    fa_bwd8_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
-                  const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse,
-                  const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
-                  float scale, float scale2, unsigned long long* __restrict__ trace) {
-  using L = BwdSmem<DH>;
-  // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
-  auto TR = [&](int it, int ev) {
-    if (trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it < 32) trace[it * 16 + ev] = clock64();
-  };
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *do_full = bar + 5, *do_empty = bar + 6,
-           *s_full = bar + 7, *dp_full = bar + 8, *tdp_free = bar + 9, *p_ready = bar + 10, *ds_ready = bar + 11,
-           *mm2_done = bar + 12, *dq_done = bar + 13, *dv_done = bar + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
-  float* lse_s = reinterpret_cast<float*>(sm + L::OFF_LSE);
-  float* del_s = reinterpret_cast<float*>(sm + L::OFF_DEL);
-
-  const int n_q = S / BQ;
-  // head-major order (Q, dO of one head stay in L2), heaviest key tiles (most query tiles) first in a head
-  const int jt = static_cast<int>(blockIdx.x % n_q);
-  const int h = static_cast<int>(blockIdx.x / n_q);
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int n_it = n_q - jt;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023) __trap();  // SW128 tiles need a 1024-byte aligned base
-    tma_prefetch(&tm);
-    tma_prefetch(&tmdo);
-    tma_prefetch(&tmdq);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-    }
-    mbar_init(do_full, 1);
-    mbar_init(do_empty, 1);
-    mbar_init(s_full, 1);
-    mbar_init(dp_full, 1);
-    mbar_init(tdp_free, 128);
-    mbar_init(p_ready, 256);
-    mbar_init(ds_ready, 256);
-    mbar_init(mm2_done, 1);
-    mbar_init(dq_done, 1);
-    mbar_init(dv_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 13) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 256 + DH;
-
-  // register budgets per warpgroup (setmaxnreg is warpgroup-aligned and must dominate each role's code)
-  if (warp >= 12) {
-   asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-   if (warp == 12) {
-    if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * L::QB);
-      for (int a = 0; a < DH / 64; ++a) {
-        tma_load_2d(sm + L::OFF_K + a * ATOM, &tm, kv_full, H + h * DH + a * 64, row0 + jt * BQ);
-        tma_load_2d(sm + L::OFF_V + a * ATOM, &tm, kv_full, 2 * H + h * DH + a * 64, row0 + jt * BQ);
-      }
-      for (int it = 0; it < n_it; ++it) {
-        const int i = jt + it, st = it & 1;
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], L::QB + 1024);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_Q + st * L::QB + a * ATOM, &tm, &q_full[st], h * DH + a * 64, row0 + i * BQ);
-        const int64_t li = (static_cast<int64_t>(b) * nh + h) * S + i * BQ;
-        bulk_load(lse_s + st * 128, lse + li, 512, &q_full[st]);
-        bulk_load(del_s + st * 128, delta + li, 512, &q_full[st]);
-        mbar_wait(do_empty, (it & 1) ^ 1);
-        mbar_expect_tx(do_full, L::QB);
-        for (int a = 0; a < DH / 64; ++a)
-          tma_load_2d(sm + L::OFF_DO + a * ATOM, &tmdo, do_full, h * DH + a * 64, row0 + i * BQ);
-      }
-    }
-   } else if (warp == 13 || warp == 14) {
-    // two MMA issuers on SMSPs 1 and 2, each a whole warp with one elected lane issuing:
-    //   warp 9  (X): dPᵀ_i (after dQ_{i−1} was drained), then Sᵀ_{i+1} (after dV_i has read Pᵀ_i)
-    //   warp 10 (Y): dV_i (after Pᵀ_i is written), then dQ_i, dK_i (after dSᵀ_i is in smem)
-    // an SMSP that issues MMAs loses issue slots to its other warps roughly while they execute: splitting the five
-    // products over two SMSPs halves what the compute warp sharing each one loses
-    constexpr uint32_t id_s = umma_idesc_bf16(128, 128, false, false);  // Sᵀ, dPᵀ: K = d
-    constexpr uint32_t id_kv = umma_idesc_bf16(128, DH, false, true);   // dV, dK: A K-major (K = q), B MN-major
-    constexpr uint32_t id_q = umma_idesc_bf16(128, DH, true, true);     // dQ: A = dSᵀ viewed MN-major
-    const uint32_t sK = smem_u32(sm + L::OFF_K), sV = smem_u32(sm + L::OFF_V), sDS = smem_u32(sm + L::OFF_DS),
-                   sDO = smem_u32(sm + L::OFF_DO);
-    if (warp == 13) {
-      auto issue_s = [&](int it) {  // Sᵀ_it = K·Q_itᵀ into tS
-        const int st = it & 1;
-        mbar_wait(&q_full[st], (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tS, desc_k(sK, ks), desc_k(sQ, ks), id_s, ks > 0);
-        umma_commit_w(s_full);
-        TR(it, 0);
-      };
-      mbar_wait(kv_full, 0);
-      issue_s(0);
-      for (int it = 0; it < n_it; ++it) {
-        mbar_wait(do_full, it & 1);
-        if (it > 0) mbar_wait(tdp_free, (it - 1) & 1);
-        TR(it, 1);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_f16_w(tdP, desc_k(sV, ks), desc_k(sDO, ks), id_s, ks > 0);
-        umma_commit_w(dp_full);
-        if (it + 1 < n_it) {
-          mbar_wait(dv_done, it & 1);   // Sᵀ_{it+1} overwrites Pᵀ_it: only after dV_it has read it
-          issue_s(it + 1);
-        }
-      }
-    } else {
-      mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1;
-        const uint32_t sQ = smem_u32(sm + L::OFF_Q + st * L::QB);
-        mbar_wait(p_ready, it & 1);
-        mbar_wait(dp_full, it & 1);    // dPᵀ_it (issuer X) has read dO_i before dO is released below
-        TR(it, 2);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks)   // Pᵀ packed: query columns 0-63 at tS + 0.., 64-127 at tS + 64..
-          umma_f16_tmemA_w(tdV, tS + (ks >> 2) * 64 + (ks & 3) * 8, desc_mn(sDO, ks), id_kv, (it | ks) > 0);
-        umma_commit_w(do_empty);
-        umma_commit_w(dv_done);
-        mbar_wait(ds_ready, it & 1);
-        TR(it, 3);
-        // dQ_it precedes dK_it: its drain (which frees the TMEM columns dPᵀ_{it+1} needs) overlaps dK_it
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdP, desc_mn(sDS, ks), desc_mn(sK, ks), id_q, ks > 0);
-        umma_commit_w(dq_done);
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) umma_f16_w(tdK, desc_k(sDS, ks), desc_mn(sQ, ks), id_kv, (it | ks) > 0);
-        umma_commit_w(&q_empty[st]);
-        umma_commit_w(mm2_done);
-      }
-    }
-   }
-  } else if (warp < 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 144;" ::: "memory");
-    const int q4 = warp & 3, ch = warp >> 2;   // TMEM lane quarter, query-column half
-    const int t = q4 * 32 + lane;              // key row of the tile (TMEM lane)
-    const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-    uint8_t* sDS = sm + L::OFF_DS + ch * ATOM;   // dSᵀ columns 64·ch .. +63 are atom ch
-    for (int it = 0; it < n_it; ++it) {
-      const int st = it & 1;
-      const float* ls = lse_s + st * 128 + ch * 64;
-      const float* dl = del_s + st * 128 + ch * 64;
-      mbar_wait(&q_full[st], (it >> 1) & 1);   // LSE_i, δ_i landed (bulk copies on the same barrier as Q_i)
-      mbar_wait(s_full, it & 1);
-      if (threadIdx.x == 0) TR(it, 4);
-      tc_fence_after();
-      // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
-      uint32_t pk[2][16];   // Pᵀ_it of this warp's 64 columns, packed bf16, kept for the dS pass
-      auto p_pass = [&](auto diag) {
-        uint32_t uu[2][32];
-        tmem_ld32(tS + lane_off + ch * 64, uu[0]);
-        tmem_ld32(tS + lane_off + ch * 64 + 32, uu[1]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t (&pw)[16] = pk[c];
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
-            const float2 a2 = ffma2(make_float2(__uint_as_float(uu[c][k]), __uint_as_float(uu[c][k + 1])),
-                                    make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
-            float p0 = ex2(a2.x);
-            float p1 = ex2(a2.y);
-            if (decltype(diag)::value) {  // query index < key index is masked
-              if (ch * 64 + c * 32 + k < t) p0 = 0.f;
-              if (ch * 64 + c * 32 + k + 1 < t) p1 = 0.f;
-            }
-            pw[k / 2] = pack_bf16(p0, p1);
-          }
-          tmem_st16(tS + lane_off + ch * 64 + c * 16, pw);  // over Sᵀ columns this warp has already read
-        }
-      };
-      if (it == 0)
-        p_pass(std::true_type{});
-      else
-        p_pass(std::false_type{});
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_ready);
-      if (threadIdx.x == 0) TR(it, 5);
-      mbar_wait(dp_full, it & 1);
-      if (threadIdx.x == 0) TR(it, 6);
-      if (it > 0) mbar_wait(mm2_done, (it - 1) & 1);  // dSᵀ of the previous tile consumed by dK / dQ
-      if (threadIdx.x == 0) TR(it, 7);
-      tc_fence_after();
-      {
-        uint32_t uu[2][32];
-        tmem_ld32(tdP + lane_off + ch * 64, uu[0]);
-        tmem_ld32(tdP + lane_off + ch * 64 + 32, uu[1]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const uint32_t (&pp)[16] = pk[c];
-          uint32_t d[16];
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            const float2 dl2 = *reinterpret_cast<const float2*>(dl + c * 32 + k);
-            const float2 ds2 = fmul2(make_float2(bf_lo(pp[k / 2]), bf_hi(pp[k / 2])),
-                                     fadd2(make_float2(__uint_as_float(uu[c][k]), __uint_as_float(uu[c][k + 1])),
-                                           make_float2(-dl2.x, -dl2.y)));
-            d[k / 2] = pack_bf16(ds2.x, ds2.y);
-          }
-          // 32 columns = 4 × 16-byte chunks, chunk index c·4 + v of this warp's atom
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int chunk = c * 4 + v;
-            *reinterpret_cast<uint4*>(sDS + t * 128 + ((chunk ^ (t & 7)) << 4)) =
-                make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
-          }
-        }
-      }
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(ds_ready);
-      if (threadIdx.x == 0) TR(it, 8);
-      if (lane == 0 && warp < 4) TR(it, 12 + warp);   // per-warp dS done (column half 0)
-    }
-    // dK (× softmax scale) rows of this key tile from the column-half-0 warps, dV rows from the half-1 warps
-    mbar_wait(mm2_done, (n_it - 1) & 1);
-    tc_fence_after();
-    const uint32_t tsrc = ch == 0 ? tdK : tdV;
-    const float sc = ch == 0 ? scale : 1.0f;
-    bf16* dst = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + (ch == 0 ? H : 2 * H) + h * DH;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t u[32];
-      tmem_ld32(tsrc + lane_off + c * 32, u);
-      tmem_wait_ld();
-      uint4* o4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o;
-        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * sc, __uint_as_float(u[8 * v + 1]) * sc);
-        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * sc, __uint_as_float(u[8 * v + 3]) * sc);
-        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * sc, __uint_as_float(u[8 * v + 5]) * sc);
-        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * sc, __uint_as_float(u[8 * v + 7]) * sc);
-        o4[v] = o;
-      }
-    }
-    tc_fence_before();
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
-    // dQ warps 8-11: TMEM lane quarter (warp % 4) holds query rows of dQ_i
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    uint8_t* stg = sm + L::OFF_STG;
-    int rnd = 0;   // staging rounds issued so far (buffer half = rnd & 1)
-    for (int it = 0; it < n_it; ++it) {
-      const int i = jt + it;
-      mbar_wait(dq_done, it & 1);    // dQ_i complete
-      if (t == 0) TR(it, 9);
-      tc_fence_after();
-      uint32_t u[DH / 32][32];
-#pragma unroll
-      for (int c = 0; c < DH / 32; ++c) tmem_ld32(tdP + lane_off + c * 32, u[c]);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(tdp_free);                   // TMEM columns free for the next dPᵀ
-      if (t == 0) TR(it, 10);
-      // 32-column rounds through the two 16 KB halves of the staging buffer: a round waits only for the reduce
-      // issued two rounds earlier (wait_group.read 1), so writing one half overlaps the TMA read of the other
-#pragma unroll
-      for (int c = 0; c < DH / 32; ++c, ++rnd) {
-        uint8_t* buf = stg + (rnd & 1) * ATOM;
-        if (t == 0) bulk_wait_read1();
-        named_bar(2, 128);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<uint4*>(buf + t * 128 + ((j ^ (t & 7)) << 4)) =
-              make_uint4(u[c][4 * j], u[c][4 * j + 1], u[c][4 * j + 2], u[c][4 * j + 3]);
-        fence_async_smem();
-        named_bar(2, 128);
-        if (t == 0) {
-          tma_reduce_add_2d(&tmdq, buf, h * DH + c * 32, row0 + i * BQ);
-          bulk_commit();
-        }
-      }
-      if (t == 0) TR(it, 11);
-    }
-    if (t == 0) bulk_wait_all0();
-  }
-  __syncthreads();
-  if (warp == 13) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-
-
 // δ_i = Σ_d dO_id·O_id ; one warp per (row, head)
 __global__ void fa_delta_kernel(int64_t rows, int S, int nh, int dh, const bf16* __restrict__ o,
                                 const bf16* __restrict__ dout, float* __restrict__ delta,
@@ -1430,21 +1112,7 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   const float scale2 = LOG2E * scale;
   dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
   FaTrace tr;
-  static const int bwd_ver = [] {
-    const char* e = std::getenv("TAWPIPE_FA_BWD");
-    return e ? std::atoi(e) : 8;
-  }();
-  if (bwd_ver == 8) {
-    if (dh == 128) {
-      prep(fa_bwd8_kernel<128>, BwdSmem<128>::BYTES);
-      fa_bwd8_kernel<128><<<grid, 512, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh,
-                                                                  scale, scale2, tr.p);
-    } else {
-      prep(fa_bwd8_kernel<64>, BwdSmem<64>::BYTES);
-      fa_bwd8_kernel<64><<<grid, 512, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh,
-                                                                scale, scale2, tr.p);
-    }
-  } else if (dh == 128) {
+  if (dh == 128) {
     prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES);
     fa_bwd_kernel<128><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
                                                                scale2, tr.p);

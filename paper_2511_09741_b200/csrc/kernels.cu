@@ -607,6 +607,72 @@ __global__ void rmsnorm_dgamma_v8_kernel(const bf16* __restrict__ dy, const bf16
   atomicAdd(&dg_acc[blockIdx.x * 256 + threadIdx.x], v);
 }
 
+// Single-pass cross-entropy for bf16 logits, V % 8 == 0 and V ≤ 8·NT·NV: the row is read once into registers (16-byte
+// loads), max and Σexp are block reductions over the registers, and dz is written once -- one read and one write
+// of the row (the three-pass ce_kernel re-read it twice)
+template <int NT, int NV>
+__global__ void __launch_bounds__(NT) ce_v8_kernel(bf16* __restrict__ z, const int32_t* __restrict__ tgt, int V,
+                                                   float inv_denom, float* __restrict__ loss_rows) {
+  __shared__ float red[NT / 32];
+  const int64_t row = blockIdx.x;
+  bf16* zr = z + row * V;
+  const int nvec = V / 8;
+  uint4 u[NV];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = threadIdx.x + i * NT;
+    if (v < nvec) {
+      u[i] = *reinterpret_cast<const uint4*>(zr + v * 8);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        mx = fmaxf(mx, fmaxf(f.x, f.y));
+      }
+    }
+  }
+  mx = block_max<NT>(mx, red);
+  float se = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = threadIdx.x + i * NT;
+    if (v < nvec) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        se += __expf(f.x - mx) + __expf(f.y - mx);
+      }
+    }
+  }
+  se = block_sum<NT>(se, red);
+  const float lse = mx + __logf(se);
+  const int t = tgt[row];
+  if (threadIdx.x == 0) loss_rows[row] = lse - __bfloat162float(zr[t]);   // z[t] read before any dz is written
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int v = threadIdx.x + i * NT;
+    if (v < nvec) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+      float p[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        p[2 * k] = __expf(f.x - lse);
+        p[2 * k + 1] = __expf(f.y - lse);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (v * 8 + k == t) p[k] -= 1.f;
+        p[k] *= inv_denom;
+      }
+      st8(zr + v * 8, p);
+    }
+  }
+}
+
 inline unsigned grid_stride_blocks(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -725,6 +791,13 @@ void swiglu_bwd(const T* dy, const T* gu, T* dgu, int64_t rows, int I, cudaStrea
 template <typename T>
 void cross_entropy(T* logits, const int32_t* targets, int64_t rows, int V, float inv_denom, float* loss_rows,
                    cudaStream_t s) {
+  if constexpr (std::is_same<T, bf16>::value) {
+    if (V % 8 == 0 && V <= 8 * 512 * 8) {   // up to V = 32,768 in registers
+      ce_v8_kernel<512, 8><<<static_cast<unsigned>(rows), 512, 0, s>>>(logits, targets, V, inv_denom, loss_rows);
+      LAUNCHED();
+      return;
+    }
+  }
   ce_kernel<T, 512><<<static_cast<unsigned>(rows), 512, 0, s>>>(logits, targets, V, inv_denom, loss_rows);
   LAUNCHED();
 }

@@ -73,7 +73,7 @@ z = torch.randn(tc, V, device="cuda").bfloat16()
 tg = torch.randint(0, V, (tc,), device="cuda", dtype=torch.int32)
 lr = torch.empty(tc, device="cuda")
 ms = timed(lambda: T.cross_entropy(BF, tc, V, z.data_ptr(), tg.data_ptr(), 1.0 / 32768, lr.data_ptr()))
-report("ce_kernel (8192 rows, V=32000)", ms, tc * (2 * V * 2 + 4 + 4))
+report("ce_v8_kernel (single pass, 8192 rows, V=32000)", ms, tc * (2 * V * 2 + 4 + 4))
 del z
 # embedding backward at C3 (32768 positions, H = 4096, V = 32000)
 tok = torch.randint(0, V, (1, rows + 1), device="cuda", dtype=torch.int32)

@@ -30,14 +30,14 @@ __global__ void tmem_bw_kernel(int iters, int cols_per_warp, unsigned long long*
       if (MODE == 0) {
         tmem_ld32(base + c, r);
         tmem_wait_ld();
-        acc += r[it & 31];
+        acc += r[0] ^ r[13] ^ r[31];
       } else if (MODE == 1) {
         tmem_st32(base + c, r);
         tmem_wait_st();
       } else {
         tmem_ld_16x256b_x8(base + c + ((threadIdx.x & 32) ? 0 : 0), r);   // 16 lanes x 64 columns
         tmem_wait_ld();
-        acc += r[it & 31];
+        acc += r[0] ^ r[13] ^ r[31];
       }
     }
   }

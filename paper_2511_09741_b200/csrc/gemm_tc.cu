@@ -560,7 +560,11 @@ int choose_raster(int64_t num_m, int64_t num_n, int64_t rows_m, int64_t rows_n, 
     const std::string v(e);
     return v == "m" ? 1 : v == "n" ? 2 : v == "default" ? 3 : 0;
   }();
-  constexpr int64_t kL2Band = 48ll << 20, kLongK = 8ll << 20;
+  static const int64_t kL2Band = [] {   // resident band budget (TAWPIPE_GEMM_BAND_MB overrides, experiments)
+    const char* e = std::getenv("TAWPIPE_GEMM_BAND_MB");
+    return (e ? std::atoll(e) : 48ll) << 20;
+  }();
+  constexpr int64_t kLongK = 8ll << 20;
   const int64_t bm = rows_m * K * 2, bn = rows_n * K * 2;   // bytes of one M-tile band / one N-tile band
   if (force == 3 || (force == 0 && bm > kLongK && bn > kLongK)) return default_group;
   const int64_t gm = std::max<int64_t>(1, std::min<int64_t>(num_m, kL2Band / bm));

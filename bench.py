@@ -58,7 +58,7 @@ def flops_per_token(c, recompute=True):
 def traffic_for(kernel):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture (profiles/)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as fh:
             t = json.load(fh)[kernel]
         return {"traffic": t["bytes"], "traffic_per": t["per"], "traffic_source": t["source"]}
     except Exception:

@@ -562,7 +562,7 @@ int choose_raster(int64_t num_m, int64_t num_n, int64_t rows_m, int64_t rows_n, 
   }();
   static const int64_t kL2Band = [] {   // resident band budget (TAWPIPE_GEMM_BAND_MB overrides, experiments)
     const char* e = std::getenv("TAWPIPE_GEMM_BAND_MB");
-    return (e ? std::atoll(e) : 48ll) << 20;
+    return (e ? std::atoll(e) : 32ll) << 20;   // measured at the QKV shape: 16 MB 2.76 GB read, 24 1.88, 32 1.72, 48 1.93
   }();
   constexpr int64_t kLongK = 8ll << 20;
   const int64_t bm = rows_m * K * 2, bn = rows_n * K * 2;   // bytes of one M-tile band / one N-tile band

@@ -49,6 +49,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
   const float p = fmaf(fmaf(fmaf(0.0550089308f, f, 0.242210984f), f, 0.69328293f), f, 1.0f);
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
+// element k of a 32-wide chunk: emulate 3 of every 8 exponentials on the FMA pipe
 
 // packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2 / FMUL2: one issue slot for two lanes of work)
 __device__ __forceinline__ unsigned long long f2u(float2 a) {
@@ -71,26 +72,6 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   unsigned long long r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2u(a)), "l"(f2u(b)));
   return u2f(r);
-}
-
-// ex2_poly on a packed pair: 3 FFMA2 + 2 FADD2-class ops on the FMA pipe and 2 integer adds per element, no MUFU.
-// (t − 1.5·2²³) << 23 == t_bits << 23 mod 2³² because 0x4B400000 has nine trailing zero bits.
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
-  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
-  const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
-  float2 p = ffma2(make_float2(0.0550089308f, 0.0550089308f), f, make_float2(0.242210984f, 0.242210984f));
-  p = ffma2(p, f, make_float2(0.69328293f, 0.69328293f));
-  p = ffma2(p, f, make_float2(1.0f, 1.0f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-// exponentials of a pair: on the MUFU, or (EMU and one pair in every 4) on the FMA / ALU pipes
-template <int EMU>
-__device__ __forceinline__ float2 ex2_pair(float2 a, int pair) {
-  if (EMU && (pair & 3) == 3) return ex2_poly2(a);
-  return make_float2(ex2(a.x), ex2(a.y));
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -395,7 +376,7 @@ struct Fwd5Smem {
 // v5).  One issuer warp per tile keeps the two tiles' MMA streams independent.  Sustained at S = 32K, 32 heads:
 // 7.35 ms against v5's 8.4 ms (7.9 ms with a single in-order issuer for both tiles).
 //   TMEM per tile t: S/P [128t, 128t+128) as halves of 64 columns, O_t [256+128t, 384+128t)
-template <int DH, int EMU>
+template <int DH>
 __global__ void __launch_bounds__(384, 1)
     fa_fwd7_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int S,
                    int nh, float scale2) {
@@ -575,8 +556,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             const float2 a2 = ffma2(make_float2(s[c * 32 + i], s[c * 32 + i + 1]), sc2, nm2);
-            const float2 pp = ex2_pair<EMU>(a2, i >> 1);
-            const float p0 = pp.x, p1 = pp.y;
+            const float p0 = ex2(a2.x), p1 = ex2(a2.y);
             sa2[(i >> 1) & 3] = fadd2(sa2[(i >> 1) & 3], make_float2(p0, p1));
             pw[i / 2] = pack_bf16(p0, p1);
           }
@@ -648,7 +628,7 @@ struct BwdSmem {
 __device__ __forceinline__ float bf_lo(uint32_t x) { return __uint_as_float(x << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 0xFFFF0000u); }
 
-template <int DH, int EMU>
+template <int DH>
 __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three warps share SMSPs 0-2)
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
                   const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse,
@@ -824,9 +804,8 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
               const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
               const float2 a2 = ffma2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
                                       make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
-              const float2 pp = ex2_pair<EMU>(a2, k >> 1);
-              float p0 = pp.x;
-              float p1 = pp.y;
+              float p0 = ex2(a2.x);
+              float p1 = ex2(a2.y);
               if (decltype(diag)::value) {  // query index < key index is masked
                 if (c * 32 + k < t) p0 = 0.f;
                 if (c * 32 + k + 1 < t) p1 = 0.f;
@@ -1074,15 +1053,6 @@ struct FaTrace {
 
 }  // namespace
 
-// TAWPIPE_FA_EMU=0|1: one exponential pair in four on the FMA / ALU pipes (d_h = 128 kernels)
-bool fa_emu() {
-  static const bool on = [] {
-    const char* e = std::getenv("TAWPIPE_FA_EMU");
-    return e ? std::atoi(e) != 0 : true;
-  }();
-  return on;
-}
-
 bool attention_tc_supported(int S, int dh) { return S % 128 == 0 && (dh == 64 || dh == 128); }
 
 // Forward: fa_fwd7 (two query tiles per CTA) when the number of query tiles is even, else fa_fwd3.
@@ -1093,15 +1063,12 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
   const float scale2 = LOG2E / sqrtf(static_cast<float>(dh));
   if ((S / BQ) % 2 == 0) {
     dim3 grid7(static_cast<unsigned>((S / BQ / 2) * nh), static_cast<unsigned>(B));
-    if (dh == 128 && fa_emu()) {
-      prep(fa_fwd7_kernel<128, 1>, Fwd5Smem<128>::BYTES);
-      fa_fwd7_kernel<128, 1><<<grid7, 352, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
-    } else if (dh == 128) {
-      prep(fa_fwd7_kernel<128, 0>, Fwd5Smem<128>::BYTES);
-      fa_fwd7_kernel<128, 0><<<grid7, 352, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+    if (dh == 128) {
+      prep(fa_fwd7_kernel<128>, Fwd5Smem<128>::BYTES);
+      fa_fwd7_kernel<128><<<grid7, 352, Fwd5Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
     } else {
-      prep(fa_fwd7_kernel<64, 0>, Fwd5Smem<64>::BYTES);
-      fa_fwd7_kernel<64, 0><<<grid7, 352, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
+      prep(fa_fwd7_kernel<64>, Fwd5Smem<64>::BYTES);
+      fa_fwd7_kernel<64><<<grid7, 352, Fwd5Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2);
     }
   } else {
     FaTrace tr;
@@ -1145,18 +1112,14 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   const float scale2 = LOG2E * scale;
   dim3 grid(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
   FaTrace tr;
-  if (dh == 128 && fa_emu()) {
-    prep(fa_bwd_kernel<128, 1>, BwdSmem<128>::BYTES);
-    fa_bwd_kernel<128, 1><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh,
-                                                                  scale, scale2, tr.p);
-  } else if (dh == 128) {
-    prep(fa_bwd_kernel<128, 0>, BwdSmem<128>::BYTES);
-    fa_bwd_kernel<128, 0><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh,
-                                                                  scale, scale2, tr.p);
+  if (dh == 128) {
+    prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES);
+    fa_bwd_kernel<128><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
+                                                               scale2, tr.p);
   } else {
-    prep(fa_bwd_kernel<64, 0>, BwdSmem<64>::BYTES);
-    fa_bwd_kernel<64, 0><<<grid, 352, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                                scale2, tr.p);
+    prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES);
+    fa_bwd_kernel<64><<<grid, 352, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
+                                                             scale2, tr.p);
   }
   TP_CUDA(cudaGetLastError());
   fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);

@@ -15,7 +15,7 @@ dqkv = torch.empty_like(qkv); delta = torch.empty(2, nh, S, device="cuda"); acc 
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 fw, bw = [], []
 with ClockSampler(0) as clk:
-    t_end = time.time() + 12
+    t_end = time.time() + 8
     while time.time() < t_end:
         ev[0].record()
         T.attention_fwd(T.BF16, 1, S, nh, dh, qkv.data_ptr(), o.data_ptr(), lse.data_ptr())

@@ -1087,10 +1087,10 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
     dim3 grid3(static_cast<unsigned>((S / BQ) * nh), static_cast<unsigned>(B));
     if (dh == 128) {
       prep(fa_fwd3_kernel<128>, Fwd3Smem<128>::BYTES);
-      fa_fwd3_kernel<128><<<grid3, 224, Fwd3Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2, tr.p, fa_dbg());
+      fa_fwd3_kernel<128><<<grid3, 224, Fwd3Smem<128>::BYTES, s>>>(tm, o, lse, S, nh, scale2, tr.p);
     } else {
       prep(fa_fwd3_kernel<64>, Fwd3Smem<64>::BYTES);
-      fa_fwd3_kernel<64><<<grid3, 224, Fwd3Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2, tr.p, fa_dbg());
+      fa_fwd3_kernel<64><<<grid3, 224, Fwd3Smem<64>::BYTES, s>>>(tm, o, lse, S, nh, scale2, tr.p);
     }
     TP_CUDA(cudaGetLastError());
     static const char* names[16] = {"mma:p_ready", "mma:v_full", "mma:issued", "smx:s_full", "smx:p_done", nullptr};

@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
         umma_commit_w(dp_full);
         if (it + 1 < n_it) {
           mbar_wait(dv_done, it & 1);   // Sᵀ_{it+1} overwrites Pᵀ_it: only after dV_it has read it
+          if (dbg & 16) mbar_wait(ds_ready, it & 1);   // experiment: keep Sᵀ_{it+1} off the smem during the dS pass
           issue_s(it + 1);
         }
       }

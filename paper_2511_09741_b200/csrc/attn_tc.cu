@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
                   const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse,
                   const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
-                  float scale, float scale2, unsigned long long* __restrict__ trace, int dbg) {
+                  float scale, float scale2, unsigned long long* __restrict__ trace) {
   using L = BwdSmem<DH>;
   // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
   auto TR = [&](int it, int ev) {
@@ -744,7 +744,6 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
         umma_commit_w(dp_full);
         if (it + 1 < n_it) {
           mbar_wait(dv_done, it & 1);   // Sᵀ_{it+1} overwrites Pᵀ_it: only after dV_it has read it
-          if (dbg & 16) mbar_wait(ds_ready, it & 1);   // experiment: keep Sᵀ_{it+1} off the smem during the dS pass
           issue_s(it + 1);
         }
       }
@@ -802,11 +801,11 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
             uint32_t (&pw)[16] = pk[c];
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
-              const float2 l2 = (dbg & 2) ? make_float2(1.f, 1.f) : *reinterpret_cast<const float2*>(ls + c * 32 + k);
+              const float2 l2 = *reinterpret_cast<const float2*>(ls + c * 32 + k);
               const float2 a2 = ffma2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
                                       make_float2(scale2, scale2), make_float2(-l2.x, -l2.y));
-              float p0 = (dbg & 8) ? a2.x : ex2(a2.x);
-              float p1 = (dbg & 8) ? a2.y : ex2(a2.y);
+              float p0 = ex2(a2.x);
+              float p1 = ex2(a2.y);
               if (decltype(diag)::value) {  // query index < key index is masked
                 if (c * 32 + k < t) p0 = 0.f;
                 if (c * 32 + k + 1 < t) p1 = 0.f;
@@ -843,7 +842,7 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
           uint32_t d[16];
 #pragma unroll
           for (int k = 0; k < 32; k += 2) {
-            const float2 dl2 = (dbg & 2) ? make_float2(1.f, 1.f) : *reinterpret_cast<const float2*>(dl + c * 32 + k);
+            const float2 dl2 = *reinterpret_cast<const float2*>(dl + c * 32 + k);
             const float2 ds2 = fmul2(make_float2(bf_lo(pp[k / 2]), bf_hi(pp[k / 2])),
                                      fadd2(make_float2(__uint_as_float(uu[h2][k]), __uint_as_float(uu[h2][k + 1])),
                                            make_float2(-dl2.x, -dl2.y)));
@@ -852,7 +851,6 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
           // 32 columns = 4 × 16-byte chunks of atom c/2, chunk index (c%2)*4 + v
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            if (dbg & 4) break;
             const int chunk = (c & 1) * 4 + v;
             *reinterpret_cast<uint4*>(sDS + (c >> 1) * ATOM + t * 128 + ((chunk ^ (t & 7)) << 4)) =
                 make_uint4(d[4 * v], d[4 * v + 1], d[4 * v + 2], d[4 * v + 3]);
@@ -917,7 +915,6 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
       // issued two rounds earlier (wait_group.read 1), so writing one half overlaps the TMA read of the other
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c, ++rnd) {
-        if (dbg & 1) break;
         uint8_t* buf = stg + (rnd & 1) * ATOM;
         if (t == 0) bulk_wait_read1();
         named_bar(2, 128);
@@ -1056,16 +1053,6 @@ struct FaTrace {
 
 }  // namespace
 
-// TAWPIPE_FA_DBG (ablation experiments, WRONG RESULTS): 1 skip dQ staging + reduce, 2 LSE/δ from registers,
-// 4 skip dS smem stores, 8 skip the exponentials
-int fa_dbg() {
-  static const int v = [] {
-    const char* e = std::getenv("TAWPIPE_FA_DBG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 bool attention_tc_supported(int S, int dh) { return S % 128 == 0 && (dh == 64 || dh == 128); }
 
 // Forward: fa_fwd7 (two query tiles per CTA) when the number of query tiles is even, else fa_fwd3.
@@ -1128,11 +1115,11 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   if (dh == 128) {
     prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES);
     fa_bwd_kernel<128><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                               scale2, tr.p, fa_dbg());
+                                                               scale2, tr.p);
   } else {
     prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES);
     fa_bwd_kernel<64><<<grid, 352, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                             scale2, tr.p, fa_dbg());
+                                                             scale2, tr.p);
   }
   TP_CUDA(cudaGetLastError());
   fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);

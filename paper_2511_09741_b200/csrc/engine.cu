@@ -1384,7 +1384,17 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   // ---- streams, events, communicators
   TP_CUDA(cudaStreamCreateWithFlags(&c.cs, cudaStreamNonBlocking));
   TP_CUDA(cudaStreamCreateWithFlags(&c.ws, cudaStreamNonBlocking));
-  TP_CUDA(cudaStreamCreateWithFlags(&c.gs, cudaStreamNonBlocking));
+  {
+    // TAWPIPE_GS_PRIORITY=1: the gradient stream at the highest priority, so its (short, memory-bound) reduction and
+    // AdamW blocks are dispatched ahead of the compute stream's pending attention / GEMM blocks
+    const char* e = std::getenv("TAWPIPE_GS_PRIORITY");
+    int lo = 0, hi = 0;
+    TP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (e && std::atoi(e) != 0)
+      TP_CUDA(cudaStreamCreateWithPriority(&c.gs, cudaStreamNonBlocking, hi));
+    else
+      TP_CUDA(cudaStreamCreateWithFlags(&c.gs, cudaStreamNonBlocking));
+  }
   for (int i = 0; i < 2; ++i) {
     TP_CUDA(cudaEventCreateWithFlags(&c.w_ready[i], cudaEventDisableTiming));
     TP_CUDA(cudaEventCreateWithFlags(&c.w_free[i], cudaEventDisableTiming));

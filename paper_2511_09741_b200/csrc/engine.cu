@@ -145,6 +145,7 @@ struct Ctx {
   uint32_t wprev[2] = {0, 0}, gprev[2] = {0, 0}, pprev[4] = {0, 0, 0, 0};
   int pprev_owner[4] = {0, 0, 0, 0};      // the rank that read the previous partial in that slot
   double nvl_w_bytes = 0, nvl_g_bytes = 0;   // bytes this rank pulled / read over NVLink in the last step
+  std::vector<uint32_t> sig_expect;       // [SK_* · kSigRanks + src]: the last value each peer must have written
   // events
   cudaEvent_t w_ready[2], w_free[2], g_ready[2], g_free[2], evE, evF, evGF, evGE, ev_s0, ev_s1, ev_ws0, ev_ws1,
       ev_gs0, ev_gs1;
@@ -678,11 +679,20 @@ inline const uint32_t* my_flag(int kind, int src_rank) { return g->sig + kind * 
 inline char* peer_ptr(int rank, int buf, int64_t bytes) { return static_cast<char*>(g->peer[rank][buf]) + bytes; }
 
 // tell every other member of my group: flag `kind` from me is now `seq`
+// Group members run the same gather / reduction sequence over the same ownership, so what I send a member of a
+// group-level kind is exactly what it sends me: record it as the value my flag from that member must end at.
+void expect_flag(int kind, int src, uint32_t seq) {
+  uint32_t& e = g->sig_expect[static_cast<size_t>(kind) * kSigRanks + src];
+  e = std::max(e, seq);
+}
 void signal_group(int kind, uint32_t seq, cudaStream_t s) {
   uint32_t* f[kMaxSignalTargets];
   int n = 0;
   for (int jj = 0; jj < g->G; ++jj)
-    if (jj != g->j) f[n++] = flag_at(rank_of(g->k, jj), kind, g->rank);
+    if (jj != g->j) {
+      f[n++] = flag_at(rank_of(g->k, jj), kind, g->rank);
+      expect_flag(kind, rank_of(g->k, jj), seq);
+    }
   signal_peers(f, n, seq, s);
 }
 void wait_group_peers(int kind, uint32_t seq, cudaStream_t s) {
@@ -773,6 +783,7 @@ void reduce_p2p(int uid, int slot, float* gacc) {
         }
       } else {
         wait_flag(my_flag(SK_PREADY, rank_of(kk, c.j)), seq, s);
+        expect_flag(SK_PREADY, rank_of(kk, c.j), seq);
         src.p[n++] = peer_ptr(rank_of(kk, c.j), PB_PART, part_b);
       }
       src.group_end[src.n_groups++] = n;
@@ -799,6 +810,7 @@ void reduce_p2p(int uid, int slot, float* gacc) {
     if (c.pprev[ps]) wait_flag(my_flag(SK_PDONE, c.pprev_owner[ps]), c.pprev[ps], s);
     c.pprev[ps] = seq;
     c.pprev_owner[ps] = owner;
+    expect_flag(SK_PDONE, owner, seq);   // the owner acknowledges every partial it reads
     PartialSources src;
     for (int jj = 0; jj < c.G; ++jj) src.p[src.n++] = reinterpret_cast<const float*>(peer_ptr(rank_of(c.k, jj), gb, stripe_b));
     {
@@ -1055,6 +1067,26 @@ void build_trace_json(float step_ms) {
   c.trace_json.swap(out);
 }
 
+// Invariant of the peer path, checked after every step (the step ends with a device-wide barrier, so no flag can
+// still be in flight): every flag a peer writes into this rank ends at exactly the last sequence number of its
+// kind that peer had to send.  A lost, duplicated or mis-numbered signal -- a protocol race -- raises
+// TAWPIPE_EINVARIANT instead of silently mis-ordering a later step.
+void check_flags() {
+  Ctx& c = *g;
+  std::vector<uint32_t> host(static_cast<size_t>(SK_N) * kSigRanks);
+  TP_CUDA(cudaMemcpy(host.data(), c.sig, host.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  static const char* names[SK_N] = {"RAIL", "WDONE", "GREADY", "GDONE", "PREADY", "PDONE"};
+  for (int kind = 0; kind < SK_N; ++kind)
+    for (int src = 0; src < c.P; ++src) {
+      const size_t i = static_cast<size_t>(kind) * kSigRanks + src;
+      if (c.sig_expect[i] != 0 && host[i] != c.sig_expect[i])
+        throw Error(TAWPIPE_EINVARIANT, std::string("peer flag ") + names[kind] + " from rank " + std::to_string(src) +
+                                            " is " + std::to_string(host[i]) + ", expected " +
+                                            std::to_string(c.sig_expect[i]) + " at the end of step " +
+                                            std::to_string(c.step_t));
+    }
+}
+
 // ------------------------------------------------------------------------------------ one iteration
 double run_step(const int32_t* tokens, bool device_tokens) {
   Ctx& c = *g;
@@ -1186,6 +1218,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   TP_CUDA(cudaEventRecord(c.ev_s1, c.cs));
   TP_CUDA(cudaStreamSynchronize(c.cs));
   TP_CUDA(cudaDeviceSynchronize());
+  if (c.p2p) check_flags();
   // ---- stats
   std::memset(c.stats, 0, sizeof(c.stats));
   float ms = 0.f;
@@ -1324,6 +1357,7 @@ void setup_p2p() {
   TP_CHECK(c.P <= kSigRanks && c.G <= kMaxPartialSources && c.G - 1 + c.D - 1 <= kMaxSignalTargets && c.G * 1 + c.D <= 16,
            TAWPIPE_ECONFIG, "peer path: at most 64 ranks, 8 members per group, 16 gradient sources");
   c.sig = static_cast<uint32_t*>(dmalloc(SK_N * kSigRanks * sizeof(uint32_t)));
+  c.sig_expect.assign(static_cast<size_t>(SK_N) * kSigRanks, 0);
   TP_CUDA(cudaMemsetAsync(c.sig, 0, SK_N * kSigRanks * sizeof(uint32_t), c.cs));
   if (c.D > 1) c.part = dmalloc(4 * c.max_s * c.esz);
   std::vector<void*> local(PB_N, nullptr);

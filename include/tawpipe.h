@@ -210,6 +210,13 @@ int tawpipe_gemm(int dtype, int64_t M, int64_t N, int64_t K,
                  void* C, int64_t c_ld, int c_f32, int accumulate,
                  const void* R, void* stream);
 
+/* bf16 QKV projection with RoPE in the epilogue (the step's a5): qkv [M, N] = x·Wᵀ (x [M, K], W [N, K], both K-major),
+ * then output columns [0, rope_cols) -- the q | k blocks, d_h-wide heads -- rotate-half rotated by p·θ_i with
+ * p = row mod S and θ_i = theta^(−2i/d_h) (tables built as tawpipe_init builds them).  M, N mod 128, K mod 64,
+ * d_h % 64 == 0, rope_cols % 256 == 0.  Synchronous. */
+int tawpipe_gemm_rope(int64_t M, int64_t N, int64_t K, const void* x, const void* w, void* qkv, int S, int d_h,
+                      float theta, int64_t rope_cols, void* stream);
+
 /* bf16 gate/up projection with the SwiGLU forward in the epilogue (the step's a5 MLP):
  * [u | w] = x·W_guᵀ (x [M,K], W_gu [2I,K] = [W_gate ; W_up]); y [M,I] = SiLU(u)⊙w computed from the fp32
  * accumulators; gu [M,2I] (nullable) receives [u | w] in bf16.  M, 2I mod 256 or 128, K mod 64 == 0. */
@@ -234,6 +241,13 @@ int tawpipe_attention_fwd(int dtype, int B, int S, int n_h, int d_h,
 int tawpipe_attention_bwd(int dtype, int B, int S, int n_h, int d_h,
                           const void* qkv, const void* o, const float* lse, const void* do_,
                           void* dqkv, float* scratch, float* dq_acc, void* stream);
+
+/* Causal attention backward followed by the inverse RoPE of dq and dk (the step's order: dq, dk w.r.t. the UN-roped
+ * q, k, rotated back by −p·θ_i with θ_i = theta^(−2i/d_h)); on the bf16 tcgen05 path the rotation is fused into the
+ * kernel's dq conversion and dK epilogue, as in tawpipe_step.  Arguments as tawpipe_attention_bwd.  Synchronous. */
+int tawpipe_attention_bwd_rope(int dtype, int B, int S, int n_h, int d_h, float theta,
+                               const void* qkv, const void* o, const float* lse, const void* do_,
+                               void* dqkv, float* scratch, float* dq_acc, void* stream);
 
 /* RMSNorm forward: y[r] = x[r]·rstd[r]⊙γ, rstd[r] = (mean_H(x[r]²) + eps)^(−1/2);
  * x, y [rows, H] (dtype), γ [H] (dtype), rstd [rows] fp32. */

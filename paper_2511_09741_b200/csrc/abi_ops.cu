@@ -47,6 +47,34 @@ int tawpipe_gemm(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int6
   });
 }
 
+int tawpipe_gemm_rope(int64_t M, int64_t N, int64_t K, const void* x, const void* w, void* qkv, int S, int d_h,
+                      float theta, int64_t rope_cols, void* stream) {
+  return guarded([&] {
+    TP_CHECK(S >= 1 && d_h >= 64 && d_h % 64 == 0, TAWPIPE_ECONFIG, "gemm_rope: S >= 1, d_h % 64 == 0");
+    cudaStream_t s = as_stream(stream);
+    std::vector<float> cs, sn;
+    rope_tables_host(S, d_h, theta, cs, sn);
+    const int half = d_h / 2;
+    std::vector<float> both(static_cast<size_t>(S) * d_h);
+    for (int p = 0; p < S; ++p)
+      for (int i = 0; i < half; ++i) {
+        both[static_cast<size_t>(p) * d_h + i] = cs[static_cast<size_t>(p) * half + i];
+        both[static_cast<size_t>(p) * d_h + half + i] = sn[static_cast<size_t>(p) * half + i];
+      }
+    float* d = nullptr;
+    TP_CUDA(cudaMallocAsync(&d, both.size() * 4, s));
+    TP_CUDA(cudaMemcpyAsync(d, both.data(), both.size() * 4, cudaMemcpyHostToDevice, s));
+    GemmArgs a{M, N, K, x, K, true, w, K, true, qkv, N, false, false, nullptr};
+    a.rope.cs = d;
+    a.rope.S = S;
+    a.rope.dh = d_h;
+    a.rope.cols = rope_cols;
+    gemm_tc_bf16(a, s);
+    TP_CUDA(cudaFreeAsync(d, s));
+    TP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int tawpipe_gemm_swiglu(int64_t M, int64_t I, int64_t K, const void* x, const void* w_gu, void* gu, void* y,
                         void* stream) {
   return guarded([&] {
@@ -100,6 +128,37 @@ int tawpipe_attention_bwd(int dtype, int B, int S, int n_h, int d_h, const void*
     else
       attention_bwd_simt<bf16>(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv,
                                scratch, s);
+  });
+}
+
+int tawpipe_attention_bwd_rope(int dtype, int B, int S, int n_h, int d_h, float theta, const void* qkv, const void* o,
+                               const float* lse, const void* do_, void* dqkv, float* scratch, float* dq_acc,
+                               void* stream) {
+  return guarded([&] {
+    check_dtype(dtype);
+    cudaStream_t s = as_stream(stream);
+    std::vector<float> cs, sn;
+    rope_tables_host(S, d_h, theta, cs, sn);
+    float *dc = nullptr, *dsn = nullptr;
+    TP_CUDA(cudaMallocAsync(&dc, cs.size() * 4, s));
+    TP_CUDA(cudaMallocAsync(&dsn, sn.size() * 4, s));
+    TP_CUDA(cudaMemcpyAsync(dc, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, s));
+    TP_CUDA(cudaMemcpyAsync(dsn, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, s));
+    if (dtype == TAWPIPE_BF16 && attention_tc_supported(S, d_h) && !env_is("TAWPIPE_ATTN", "simt")) {
+      attention_bwd_tc(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv, scratch,
+                       dq_acc, s, dc, dsn);
+    } else if (dtype == TAWPIPE_BF16) {
+      attention_bwd_simt<bf16>(B, S, n_h, d_h, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)do_, (bf16*)dqkv,
+                               scratch, s);
+      rope_apply<bf16>((bf16*)dqkv, B, S, n_h, d_h, dc, dsn, true, 2, s);
+    } else {
+      attention_bwd_simt<float>(B, S, n_h, d_h, (const float*)qkv, (const float*)o, lse, (const float*)do_,
+                                (float*)dqkv, scratch, s);
+      rope_apply<float>((float*)dqkv, B, S, n_h, d_h, dc, dsn, true, 2, s);
+    }
+    TP_CUDA(cudaFreeAsync(dc, s));
+    TP_CUDA(cudaFreeAsync(dsn, s));
+    TP_CUDA(cudaStreamSynchronize(s));
   });
 }
 

@@ -633,7 +633,8 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
     fa_bwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmdo,
                   const __grid_constant__ CUtensorMap tmdq, const float* __restrict__ lse,
                   const float* __restrict__ delta, float* __restrict__ dq_acc, bf16* __restrict__ dqkv, int S, int nh,
-                  float scale, float scale2, unsigned long long* __restrict__ trace) {
+                  float scale, float scale2, unsigned long long* __restrict__ trace, const float* __restrict__ rcos,
+                  const float* __restrict__ rsin) {
   using L = BwdSmem<DH>;
   // debug timeline (CTA 0 only, first 32 iterations): trace[it * 16 + event] = clock64()
   auto TR = [&](int it, int ev) {
@@ -863,33 +864,61 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
       if (t == 0) TR(it, 8);
       if (lane == 0) TR(it, 12 + warp);   // per-warp dS done
     }
-    // dK (× softmax scale) and dV rows of this key tile
+    // dK (× softmax scale) and dV rows of this key tile.  With RoPE tables (rcos != nullptr) dK is also rotated back
+    // by −p·θ_i (the inverse RoPE of the step: dk_i = dy_i cos + dy_{i+d/2} sin, dk_{i+d/2} =
+    // dy_{i+d/2} cos − dy_i sin), so no separate pass re-reads dqkv: columns c and c + d/2 are loaded together.
     mbar_wait(mm2_done, (n_it - 1) & 1);
     tc_fence_after();
     bf16* dkp = dqkv + static_cast<int64_t>(row0 + jt * BQ + t) * 3 * H + H + h * DH;
     bf16* dvp = dkp + H;
+    auto st32 = [&](bf16* dst, const float* f) {   // 32 fp32 -> 32 bf16, four 16-byte stores
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        d4[v] = make_uint4(pack_bf16(f[8 * v + 0], f[8 * v + 1]), pack_bf16(f[8 * v + 2], f[8 * v + 3]),
+                           pack_bf16(f[8 * v + 4], f[8 * v + 5]), pack_bf16(f[8 * v + 6], f[8 * v + 7]));
+    };
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t u[32], w[32];
-      tmem_ld32(tdK + lane_off + c * 32, u);
+    for (int c = 0; c < DH / 32; ++c) {   // dV
+      uint32_t w[32];
       tmem_ld32(tdV + lane_off + c * 32, w);
       tmem_wait_ld();
-      uint4* k4 = reinterpret_cast<uint4*>(dkp + c * 32);
-      uint4* v4 = reinterpret_cast<uint4*>(dvp + c * 32);
+      float f[32];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o, o2;
-        o.x = pack_bf16(__uint_as_float(u[8 * v + 0]) * scale, __uint_as_float(u[8 * v + 1]) * scale);
-        o.y = pack_bf16(__uint_as_float(u[8 * v + 2]) * scale, __uint_as_float(u[8 * v + 3]) * scale);
-        o.z = pack_bf16(__uint_as_float(u[8 * v + 4]) * scale, __uint_as_float(u[8 * v + 5]) * scale);
-        o.w = pack_bf16(__uint_as_float(u[8 * v + 6]) * scale, __uint_as_float(u[8 * v + 7]) * scale);
-        o2.x = pack_bf16(__uint_as_float(w[8 * v + 0]), __uint_as_float(w[8 * v + 1]));
-        o2.y = pack_bf16(__uint_as_float(w[8 * v + 2]), __uint_as_float(w[8 * v + 3]));
-        o2.z = pack_bf16(__uint_as_float(w[8 * v + 4]), __uint_as_float(w[8 * v + 5]));
-        o2.w = pack_bf16(__uint_as_float(w[8 * v + 6]), __uint_as_float(w[8 * v + 7]));
-        k4[v] = o;
-        v4[v] = o2;
+      for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(w[e]);
+      st32(dvp + c * 32, f);
+    }
+    constexpr int HALF = DH / 2;
+    const float* cpos = rcos ? rcos + static_cast<int64_t>(jt * BQ + t) * HALF : nullptr;
+    const float* spos = rsin ? rsin + static_cast<int64_t>(jt * BQ + t) * HALF : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < HALF / 32; ++c) {   // dK: chunk c of the first half with chunk c of the second half
+      uint32_t u1[32], u2[32];
+      tmem_ld32(tdK + lane_off + c * 32, u1);
+      tmem_ld32(tdK + lane_off + HALF + c * 32, u2);
+      tmem_wait_ld();
+      float a[32], b2[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        a[e] = __uint_as_float(u1[e]) * scale;
+        b2[e] = __uint_as_float(u2[e]) * scale;
       }
+      if (cpos) {
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 cc = reinterpret_cast<const float4*>(cpos + c * 32)[q4];
+          const float4 ss = reinterpret_cast<const float4*>(spos + c * 32)[q4];
+          const float cv[4] = {cc.x, cc.y, cc.z, cc.w}, sv[4] = {ss.x, ss.y, ss.z, ss.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x1 = a[4 * q4 + e], x2 = b2[4 * q4 + e];
+            a[4 * q4 + e] = x1 * cv[e] + x2 * sv[e];
+            b2[4 * q4 + e] = x2 * cv[e] - x1 * sv[e];
+          }
+        }
+      }
+      st32(dkp + c * 32, a);
+      st32(dkp + HALF + c * 32, b2);
     }
     tc_fence_before();
   } else if (warp < 8) {
@@ -1012,6 +1041,40 @@ __global__ void fa_dq_convert_kernel(int64_t rows, int H, const float* __restric
   }
 }
 
+// the same conversion fused with the inverse RoPE of dq (rotation by −p·θ_i, p = row mod S): each thread takes
+// 4 consecutive columns i..i+3 of the first half of a head and their partners i + d_h/2
+__global__ void fa_dq_convert_rope_kernel(int64_t rows, int S, int nh, int dh, const float* __restrict__ acc,
+                                          bf16* __restrict__ dqkv, float scale, const float* __restrict__ rcos,
+                                          const float* __restrict__ rsin) {
+  const int half = dh / 2, H = nh * dh;
+  const int64_t per_row = static_cast<int64_t>(nh) * half / 4;
+  const int64_t n = rows * per_row;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / per_row;
+    const int q = static_cast<int>(i % per_row);
+    const int head = q / (half / 4), i0 = (q % (half / 4)) * 4;
+    const int64_t base = r * H + static_cast<int64_t>(head) * dh + i0;
+    const float4 x1 = *reinterpret_cast<const float4*>(acc + base);
+    const float4 x2 = *reinterpret_cast<const float4*>(acc + base + half);
+    const int64_t t = (r % S) * half + i0;
+    const float4 cc = *reinterpret_cast<const float4*>(rcos + t);
+    const float4 ss = *reinterpret_cast<const float4*>(rsin + t);
+    const float a[4] = {x1.x * scale, x1.y * scale, x1.z * scale, x1.w * scale};
+    const float b[4] = {x2.x * scale, x2.y * scale, x2.z * scale, x2.w * scale};
+    const float cv[4] = {cc.x, cc.y, cc.z, cc.w}, sv[4] = {ss.x, ss.y, ss.z, ss.w};
+    float y1[4], y2[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      y1[k] = a[k] * cv[k] + b[k] * sv[k];
+      y2[k] = b[k] * cv[k] - a[k] * sv[k];
+    }
+    bf16* d = dqkv + r * 3 * H + static_cast<int64_t>(head) * dh + i0;
+    *reinterpret_cast<uint2*>(d) = make_uint2(pack_bf16(y1[0], y1[1]), pack_bf16(y1[2], y1[3]));
+    *reinterpret_cast<uint2*>(d + half) = make_uint2(pack_bf16(y2[0], y2[1]), pack_bf16(y2[2], y2[3]));
+  }
+}
+
 // Raise the dynamic shared-memory limit of `kern` once per (kernel, device): the attribute is per device, and a
 // process may bootstrap onto another GPU after a finalize.
 template <typename K>
@@ -1091,7 +1154,8 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
 // Backward: δ / log2-domain LSE pre-pass, fa_bwd (dK, dV in TMEM; dQ reduce-added into the fp32 dq_acc), then the
 // scaled dQ conversion into dqkv.  scratch: 2·B·n_h·S floats (δ, then LSE·log2e), owned by the caller.
 void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16* o, const float* lse,
-                      const bf16* dout, bf16* dqkv, float* scratch, float* dq_acc, cudaStream_t s) {
+                      const bf16* dout, bf16* dqkv, float* scratch, float* dq_acc, cudaStream_t s, const float* rope_cos,
+                      const float* rope_sin) {
   TP_CHECK(attention_tc_supported(S, dh), TAWPIPE_ECONFIG, "tcgen05 attention: S % 128 == 0, d_h in {64, 128}");
   TP_CHECK(dq_acc != nullptr && scratch != nullptr, TAWPIPE_ECONFIG,
            "tcgen05 attention backward needs the δ/LSE scratch and the fp32 dq accumulator");
@@ -1115,14 +1179,17 @@ void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16*
   if (dh == 128) {
     prep(fa_bwd_kernel<128>, BwdSmem<128>::BYTES);
     fa_bwd_kernel<128><<<grid, 352, BwdSmem<128>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                               scale2, tr.p);
+                                                               scale2, tr.p, rope_cos, rope_sin);
   } else {
     prep(fa_bwd_kernel<64>, BwdSmem<64>::BYTES);
     fa_bwd_kernel<64><<<grid, 352, BwdSmem<64>::BYTES, s>>>(tm, tmdo, tmdq, lse2, delta, dq_acc, dqkv, S, nh, scale,
-                                                             scale2, tr.p);
+                                                             scale2, tr.p, rope_cos, rope_sin);
   }
   TP_CUDA(cudaGetLastError());
-  fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
+  if (rope_cos)
+    fa_dq_convert_rope_kernel<<<148 * 8, 256, 0, s>>>(rows, S, nh, dh, dq_acc, dqkv, scale, rope_cos, rope_sin);
+  else
+    fa_dq_convert_kernel<<<148 * 8, 256, 0, s>>>(rows, H, dq_acc, dqkv, scale);
   TP_CUDA(cudaGetLastError());
   static const char* names[16] = {"mma:S_issued", "mma:dO+tdp_free", "mma:p_ready", "mma:ds_ready", "cmp:s_full",
                                   "cmp:p_done", "cmp:dp_full", "cmp:mm2_prev", "cmp:ds_done", "dq:mm2_done",

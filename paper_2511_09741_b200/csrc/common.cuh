@@ -52,6 +52,13 @@ struct KernelStats {
 extern KernelStats g_kstats;
 
 // ---------------------------------------------------------------- GEMM (gemm_tc.cu / gemm_simt.cu)
+// RoPE in the bf16 epilogue of the QKV projection: output columns [0, cols) (q | k) are rotated per d_h-wide head;
+// cs = [S][d_h] fp32 with cos(p·θ_i) in [0, d_h/2) and sin in [d_h/2, d_h); cs == nullptr: no RoPE
+struct RopeEpi {
+  const float* cs = nullptr;
+  int S = 0, dh = 0;
+  int64_t cols = 0;
+};
 struct GemmArgs {
   int64_t M, N, K;
   const void* A;
@@ -69,6 +76,7 @@ struct GemmArgs {
   void* aux = nullptr;
   int64_t ldx = 0;
   int64_t I = 0;
+  RopeEpi rope{};
 };
 void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s);   // tcgen05 + TMA + TMEM
 template <typename T>
@@ -81,9 +89,11 @@ template <typename T>
 void attention_bwd_simt(int B, int S, int nh, int dh, const T* qkv, const T* o, const float* lse, const T* dout,
                         T* dqkv, float* delta, cudaStream_t s);
 void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, float* lse, cudaStream_t s);
-// scratch: 2·B·n_h·S floats (δ and the log2-domain LSE); dq_acc: B·S·H floats
+// scratch: 2·B·n_h·S floats (δ and the log2-domain LSE); dq_acc: B·S·H floats.  With RoPE tables ([S][d_h/2] fp32,
+// nullable) dq and dk are also rotated back by −p·θ (the inverse RoPE fused into the dq conversion and the dK epilogue)
 void attention_bwd_tc(int B, int S, int nh, int dh, const bf16* qkv, const bf16* o, const float* lse,
-                      const bf16* dout, bf16* dqkv, float* scratch, float* dq_acc, cudaStream_t s);
+                      const bf16* dout, bf16* dqkv, float* scratch, float* dq_acc, cudaStream_t s,
+                      const float* rope_cos = nullptr, const float* rope_sin = nullptr);
 bool attention_tc_supported(int S, int dh);
 
 // ---------------------------------------------------------------- elementwise / norm / loss / optimizer

@@ -131,6 +131,7 @@ struct Ctx {
   int64_t Tc = 0;
   int32_t *d_tok = nullptr, *d_in = nullptr, *d_tgt = nullptr, *h_tok = nullptr;
   float *cosT = nullptr, *sinT = nullptr;
+  float* rope_cs = nullptr;   // [S][d_h]: cos | sin per position, for the RoPE epilogue of the QKV GEMM (bf16 path)
   double* d_loss = nullptr;
   double* h_loss = nullptr;
   uint64_t ledger[TAWPIPE_LEDGER_N] = {};
@@ -313,9 +314,9 @@ void attn_bwd(const void* qkv, const void* o, const float* lse, const void* dout
   if (!g->bf)
     attention_bwd_simt<float>(g->Bm, g->S, g->nh, g->dh, (const float*)qkv, (const float*)o, lse, (const float*)dout,
                               (float*)dqkv, g->delta, s);
-  else if (use_tc_attention())
+  else if (use_tc_attention())   // the inverse RoPE of dq / dk is fused into the kernel's dq and dK outputs
     attention_bwd_tc(g->Bm, g->S, g->nh, g->dh, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)dout,
-                     (bf16*)dqkv, g->delta, g->dq_acc, s);
+                     (bf16*)dqkv, g->delta, g->dq_acc, s, g->cosT, g->sinT);
   else
     attention_bwd_simt<bf16>(g->Bm, g->S, g->nh, g->dh, (const bf16*)qkv, (const bf16*)o, lse, (const bf16*)dout,
                              (bf16*)dqkv, g->delta, s);
@@ -891,8 +892,18 @@ void layer_forward(int l, int mb, void* W, bool write_out) {
   double work = 0;
   k_rmsnorm_fwd(hin, w.attn_norm, A.a, A.r1, T, s);
   if (!(skip & KEEP_QKV)) {
-    gemm(T, 3 * H, H, A.a, H, true, w.wqkv, H, true, A.qkv, 3 * H, false, false, nullptr, s);
-    k_rope(A.qkv, false, s);
+    if (g->rope_cs != nullptr) {   // bf16 tcgen05 path: RoPE of q | k applied in the GEMM's epilogue
+      GemmArgs a{T, 3 * H, H, A.a, H, true, w.wqkv, H, true, A.qkv, 3 * H, false, false, nullptr};
+      a.rope.cs = g->rope_cs;
+      a.rope.S = g->S;
+      a.rope.dh = g->dh;
+      a.rope.cols = 2 * H;
+      Timed t(s, 0, 2.0 * T * 3 * H * H);
+      gemm_tc_bf16(a, s);
+    } else {
+      gemm(T, 3 * H, H, A.a, H, true, w.wqkv, H, true, A.qkv, 3 * H, false, false, nullptr, s);
+      k_rope(A.qkv, false, s);
+    }
     work += 2.0 * T * 3 * H * H;
   }
   if (!(skip & KEEP_ATTN)) {
@@ -972,7 +983,7 @@ void layer_backward(int l, int mb, void* W, float* G_) {
   gemm(H, H, T, g->dh1, H, false, A.o, H, false, go, H, true, true, nullptr, s);
   gemm(T, H, H, g->dh1, H, true, w.wo, H, false, g->dO, H, false, false, nullptr, s);
   attn_bwd(A.qkv, A.o, A.lse, g->dO, g->dqkv, s);
-  k_rope(g->dqkv, true, s);
+  if (!use_tc_attention()) k_rope(g->dqkv, true, s);   // the tcgen05 backward applies it in its epilogues
   gemm(3 * H, H, T, g->dqkv, 3 * H, false, A.a, H, false, gq, H, true, true, nullptr, s);
   gemm(T, H, 3 * H, g->dqkv, 3 * H, true, w.wqkv, H, false, g->da, H, false, false, nullptr, s);
   k_rmsnorm_bwd(g->da, hin, w.attn_norm, A.r1, g->dh1, dh, G_, T, s);
@@ -1523,6 +1534,17 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
     c.sinT = (float*)dmalloc(sn.size() * 4);
     TP_CUDA(cudaMemcpyAsync(c.cosT, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, c.cs));
     TP_CUDA(cudaMemcpyAsync(c.sinT, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, c.cs));
+    if (c.bf && !gemm_force_simt() && (2 * c.H) % 256 == 0 && c.dh % 64 == 0) {
+      const int half = c.dh / 2;
+      std::vector<float> both(static_cast<size_t>(c.S) * c.dh);
+      for (int p = 0; p < c.S; ++p)
+        for (int i = 0; i < half; ++i) {
+          both[static_cast<size_t>(p) * c.dh + i] = cs[static_cast<size_t>(p) * half + i];
+          both[static_cast<size_t>(p) * c.dh + half + i] = sn[static_cast<size_t>(p) * half + i];
+        }
+      c.rope_cs = (float*)dmalloc(both.size() * 4);
+      TP_CUDA(cudaMemcpyAsync(c.rope_cs, both.data(), both.size() * 4, cudaMemcpyHostToDevice, c.cs));
+    }
     TP_CUDA(cudaStreamSynchronize(c.cs));
   }
   // ---- selective checkpointing (ckpt = 1): keep activations level by level while device memory allows

@@ -54,7 +54,47 @@ __device__ __forceinline__ float silu_sig(float u) { return 1.f / (1.f + __expf(
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int64_t row, int nb, void* __restrict__ C, int64_t ldc,
                                               const bf16* __restrict__ R, void* __restrict__ aux, int64_t ldx,
-                                              int64_t I) {
+                                              int64_t I, const RopeEpi& rope) {
+  if (EPI == EPI_BF16 && rope.cs != nullptr && static_cast<int64_t>(nb) * BN < rope.cols) {
+    // RoPE of the QKV projection in its epilogue (rotate-half, angle p·θ_i with p = row mod S): the tile holds whole
+    // heads (BN and the head width divide each other's multiples: heads are d_h-aligned, tiles BN-aligned), so the
+    // partner column i + d_h/2 of every column i is in the same tile; cos in cs[p][0, d_h/2), sin in [d_h/2, d_h)
+    const int dh = rope.dh, half = dh / 2;
+    const float* cs = rope.cs + (row % rope.S) * dh;
+#pragma unroll 1
+    for (int hb = 0; hb < BN; hb += dh) {
+#pragma unroll 1
+      for (int c = 0; c < half; c += 32) {
+        uint32_t r1[32], r2[32];
+        tmem_ld32(tbase + hb + c, r1);
+        tmem_ld32(tbase + hb + half + c, r2);
+        tmem_wait_ld();
+        float y1[32], y2[32];
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 cc = reinterpret_cast<const float4*>(cs + c)[q4];
+          const float4 ss = reinterpret_cast<const float4*>(cs + half + c)[q4];
+          const float cv[4] = {cc.x, cc.y, cc.z, cc.w}, sv[4] = {ss.x, ss.y, ss.z, ss.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float x1 = __uint_as_float(r1[4 * q4 + e]), x2 = __uint_as_float(r2[4 * q4 + e]);
+            y1[4 * q4 + e] = x1 * cv[e] - x2 * sv[e];
+            y2[4 * q4 + e] = x2 * cv[e] + x1 * sv[e];
+          }
+        }
+        bf16* d1 = reinterpret_cast<bf16*>(C) + row * ldc + static_cast<int64_t>(nb) * BN + hb + c;
+        bf16* d2 = d1 + half;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          reinterpret_cast<uint4*>(d1)[v] = make_uint4(pack_bf16(y1[8 * v], y1[8 * v + 1]), pack_bf16(y1[8 * v + 2], y1[8 * v + 3]),
+                                                       pack_bf16(y1[8 * v + 4], y1[8 * v + 5]), pack_bf16(y1[8 * v + 6], y1[8 * v + 7]));
+          reinterpret_cast<uint4*>(d2)[v] = make_uint4(pack_bf16(y2[8 * v], y2[8 * v + 1]), pack_bf16(y2[8 * v + 2], y2[8 * v + 3]),
+                                                       pack_bf16(y2[8 * v + 4], y2[8 * v + 5]), pack_bf16(y2[8 * v + 6], y2[8 * v + 7]));
+        }
+      }
+    }
+    return;
+  }
   if (EPI == EPI_SWIGLU_FWD) {
     // accumulator columns [0, BN/2) = gate u, [BN/2, BN) = up w of output features nb·BN/2 ..:
     // y = SiLU(u)·w -> aux [rows, I] ; optionally (C != nullptr) u, w -> C = gu [rows, 2I]
@@ -205,7 +245,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, void* __restrict__ C,
                    int64_t ldc, const bf16* __restrict__ R, int M, int N, int K, void* __restrict__ aux, int64_t ldx,
-                   int64_t I, int raster) {
+                   int64_t I, int raster, RopeEpi rope) {
   using Cfg = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -320,7 +360,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int64_t row = static_cast<int64_t>(mb) * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      epilogue_tile<BN, EPI>(tbase, row, nb, C, ldc, R, aux, ldx, I);
+      epilogue_tile<BN, EPI>(tbase, row, nb, C, ldc, R, aux, ldx, I, rope);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -359,7 +399,7 @@ template <bool A_MN, bool B_MN, int EPI, int NSTAGE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     void* __restrict__ C, int64_t ldc, const bf16* __restrict__ R, int M, int N, int K,
-                    void* __restrict__ aux, int64_t ldx, int64_t I, int raster) {
+                    void* __restrict__ aux, int64_t ldx, int64_t I, int raster, RopeEpi rope) {
   using Cfg = Gemm2Cfg<NSTAGE>;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -487,7 +527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       tc_fence_after();
       const int64_t row = static_cast<int64_t>(mb) * 2 * BM + rank * BM + q * 32 + lane;
       const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      epilogue_tile<BN, EPI>(tbase, row, nb, C, ldc, R, aux, ldx, I);
+      epilogue_tile<BN, EPI>(tbase, row, nb, C, ldc, R, aux, ldx, I, rope);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
@@ -606,7 +646,7 @@ void launch(const GemmArgs& g, cudaStream_t s) {
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   const int raster = choose_raster(g.M / BM, g.N / BN, BM, BN, g.K, 16);
   kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
-                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster);
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster, g.rope);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }
@@ -668,7 +708,7 @@ void launch2_n(const GemmArgs& g, cudaStream_t s) {
   const int grid = 2 * (tiles < clusters_fit ? tiles : clusters_fit);
   const int raster = choose_raster(g.M / (2 * BM), g.N / Cfg::BN, 2 * BM, Cfg::BN, g.K, 8);
   kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
-                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster);
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster, g.rope);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }
@@ -734,6 +774,9 @@ void gemm_tc_bf16(const GemmArgs& g, cudaStream_t s) {
     return;
   }
   TP_CHECK(!(g.R && g.c_f32), TAWPIPE_ECONFIG, "residual only with bf16 C");
+  TP_CHECK(g.rope.cs == nullptr || (g.epi == 0 && !g.c_f32 && !g.R && !g.accumulate && g.rope.dh % 64 == 0 &&
+                                    g.rope.cols % 256 == 0 && g.rope.S > 0),
+           TAWPIPE_ECONFIG, "RoPE epilogue: bf16 store without residual, d_h % 64 == 0, rotated columns % 256 == 0");
   TP_CHECK((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B) | reinterpret_cast<uintptr_t>(g.C)) %
                    16 == 0 &&
                g.lda % 8 == 0 && g.ldb % 8 == 0 && g.ldc % 8 == 0,

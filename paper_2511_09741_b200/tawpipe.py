@@ -77,6 +77,8 @@ def lib():
         "tawpipe_gemm": (i32, [i32, i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, i32, i32, vp, vp]),
         "tawpipe_attention_fwd": (i32, [i32, i32, i32, i32, i32, vp, vp, vp, vp]),
         "tawpipe_attention_bwd": (i32, [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "tawpipe_attention_bwd_rope": (i32, [i32, i32, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "tawpipe_gemm_rope": (i32, [i64, i64, i64, vp, vp, vp, i32, i32, f32, i64, vp]),
         "tawpipe_gemm_swiglu": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
         "tawpipe_gemm_swiglu_bwd": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
         "tawpipe_rmsnorm_fwd": (i32, [i32, i64, i32, vp, vp, f32, vp, vp, vp]),
@@ -285,6 +287,15 @@ def attention_fwd(dtype, B, S, nh, dh, qkv, o, lse, stream=None):
 def attention_bwd(dtype, B, S, nh, dh, qkv, o, lse, do, dqkv, scratch, dq_acc, stream=None):
     """scratch: 2·B·n_h·S fp32 (δ and the log2-domain LSE)."""
     _check(lib().tawpipe_attention_bwd(dtype, B, S, nh, dh, qkv, o, lse, do, dqkv, scratch, dq_acc, stream))
+
+
+def attention_bwd_rope(dtype, B, S, nh, dh, theta, qkv, o, lse, do, dqkv, scratch, dq_acc, stream=None):
+    _check(lib().tawpipe_attention_bwd_rope(dtype, B, S, nh, dh, theta, qkv, o, lse, do, dqkv, scratch, dq_acc,
+                                            stream))
+
+
+def gemm_rope(M, N, K, x, w, qkv, S, dh, theta, rope_cols, stream=None):
+    _check(lib().tawpipe_gemm_rope(M, N, K, x, w, qkv, S, dh, theta, rope_cols, stream))
 
 
 def gemm_swiglu(M, I, K, x, w_gu, gu, y, stream=None):

@@ -241,3 +241,32 @@ def test_gemm_full_size_sampled_elements(T, M, N, K, a_k, b_k, f32):
     # fp32 output: the tensor core accumulates K = 32768 products in fp32; a random-walk rounding bound
     # 4·sqrt(K)·2^-23 ≈ 8.6e-5 of the result's scale (measured 3.3e-5); bf16 output: one bf16 rounding
     assert err < (4 * np.sqrt(K) * 2.0 ** -23 if f32 else 1e-2), err
+
+
+@pytest.mark.parametrize("dtype_name,B,S,nh,dh", [("bf16", 1, 384, 2, 128), ("bf16", 2, 256, 3, 64),
+                                                  ("bf16", 1, 512, 2, 128), ("fp32", 1, 128, 4, 16)])
+def test_attention_backward_with_fused_inverse_rope_matches_oracle(T, dtype_name, B, S, nh, dh):
+    """tawpipe_attention_bwd_rope: dq / dk rotated back by −p·θ inside the tcgen05 kernel's outputs (the step's path)
+    against oracle.attention_bwd followed by oracle.rope_bwd; dv unchanged."""
+    dtype = T.BF16 if dtype_name == "bf16" else T.FP32
+    tq, tdo = attn_case(B, S, nh, dh, 13, torch.bfloat16 if dtype == T.BF16 else torch.float32)
+    H = nh * dh
+    o = torch.empty((B * S, H), dtype=tq.dtype, device="cuda")
+    lse = torch.empty((B, nh, S), dtype=torch.float32, device="cuda")
+    T.attention_fwd(dtype, B, S, nh, dh, tq.data_ptr(), o.data_ptr(), lse.data_ptr())
+    dqkv = torch.empty_like(tq)
+    scratch = torch.empty((2, B, nh, S), dtype=torch.float32, device="cuda")
+    dq_acc = torch.empty((B * S, H), dtype=torch.float32, device="cuda")
+    T.attention_bwd_rope(dtype, B, S, nh, dh, 10000.0, tq.data_ptr(), o.data_ptr(), lse.data_ptr(), tdo.data_ptr(),
+                         dqkv.data_ptr(), scratch.data_ptr(), dq_acc.data_ptr())
+    torch.cuda.synchronize()
+    got = dqkv.double().cpu().numpy()
+    _, _, rd = oracle_attention(tq, tdo, B, S, nh, dh)
+    cos, sin = om.rope_tables(S, dh, 10000.0)
+    tol = 3e-2 if dtype == T.BF16 else 1e-4
+    for b in range(B):
+        r = slice(b * S, (b + 1) * S)
+        for blk in (0, 1):
+            ref = om.rope_bwd(rd[r, blk * H:(blk + 1) * H].reshape(S, nh, dh), cos, sin).reshape(S, H)
+            assert rel(got[r, blk * H:(blk + 1) * H], ref) < tol, (b, blk, rel(got[r, blk * H:(blk + 1) * H], ref))
+        assert rel(got[r, 2 * H:], rd[r, 2 * H:]) < tol

@@ -256,3 +256,24 @@ def test_grouped_accumulate_adamw_matches_oracle(T, name, wdt, n, groups, eps, w
         assert rel(host(m), m_r) < 1e-5 and rel(host(v), v_r) < 1e-5
         assert torch.equal(wire, master.to(tdt(wdt)))   # the wire copy is the rounded master, bit for bit
         th_r = th_new
+
+
+@pytest.mark.parametrize("M,H,nh,S", [(512, 256, 2, 256), (256, 512, 8, 128), (1024, 1024, 8, 512)])
+def test_gemm_rope_epilogue_matches_oracle(T, M, H, nh, S):
+    """QKV projection with RoPE in the tcgen05 epilogue (the bf16 step's path): q | k columns of x·Wᵀ rotated as
+    oracle.rope_fwd, v columns plain; M rows are M // S sequences (p = row mod S); CTA-pair (N % 256 == 0) shapes."""
+    dh = H // nh
+    rng = np.random.default_rng(M + H)
+    x, x64 = dev(rng.standard_normal((M, H)), BF)
+    w, w64 = dev(rng.standard_normal((3 * H, H)) / np.sqrt(H), BF)
+    qkv = torch.empty((M, 3 * H), dtype=torch.bfloat16, device="cuda")
+    T.gemm_rope(M, 3 * H, H, x.data_ptr(), w.data_ptr(), qkv.data_ptr(), S, dh, 10000.0, 2 * H)
+    got = host(qkv)
+    ref = x64 @ w64.T
+    cos, sin = om.rope_tables(S, dh, 10000.0)
+    for b in range(M // S):
+        r = slice(b * S, (b + 1) * S)
+        for blk in (0, 1):
+            rr = om.rope_fwd(ref[r, blk * H:(blk + 1) * H].reshape(S, nh, dh), cos, sin).reshape(S, H)
+            assert rel(got[r, blk * H:(blk + 1) * H], rr) < 1e-2, (b, blk)
+    assert rel(got[:, 2 * H:], ref[:, 2 * H:]) < 1e-2

@@ -773,6 +773,16 @@ void reduce_p2p(int uid, int slot, float* gacc) {
     wait_group_peers(SK_GREADY, seq, s);
   }
   if (u.owned) {
+    // emulated link (NEXT-3): the owner's rail link receives the D − 1 partials while their senders transmit, so
+    // its delay runs before it waits for them (in parallel with theirs, as the NCCL path's send / recv pair did)
+    if (emu_rail_crosses()) {
+      Timed t(s, 6, 0);
+      emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
+    }
+    if (emu_group_crosses()) {
+      Timed t(s, 6, 0);
+      emu_delay(static_cast<double>(c.G - 1) * u.s * 4, s);
+    }
     GradSources src;
     int n = 0;
     for (int kk = 0; kk < c.D; ++kk) {   // ascending group order (R16)
@@ -788,14 +798,6 @@ void reduce_p2p(int uid, int slot, float* gacc) {
         src.p[n++] = peer_ptr(rank_of(kk, c.j), PB_PART, part_b);
       }
       src.group_end[src.n_groups++] = n;
-    }
-    if (emu_rail_crosses()) {
-      Timed t(s, 6, 0);
-      emu_delay(static_cast<double>(c.D - 1) * u.s * c.esz, s);
-    }
-    if (emu_group_crosses()) {
-      Timed t(s, 6, 0);
-      emu_delay(static_cast<double>(c.G - 1) * u.s * 4, s);
     }
     adam_apply(u, src, n);
     c.nvl_g_bytes += (4.0 * (c.G - 1) + static_cast<double>(c.esz) * (c.D - 1)) * u.s;

@@ -697,6 +697,13 @@ void signal_group(int kind, uint32_t seq, cudaStream_t s) {
   signal_peers(f, n, seq, s);
 }
 void wait_group_peers(int kind, uint32_t seq, cudaStream_t s) {
+  if (g->G == 1) return;
+  if (s == g->cs && g->timing) {   // a compute-stream wait on peers is exposed communication
+    Timed t(s, 3, 0);
+    for (int jj = 0; jj < g->G; ++jj)
+      if (jj != g->j) wait_flag(my_flag(kind, rank_of(g->k, jj)), seq, s);
+    return;
+  }
   for (int jj = 0; jj < g->G; ++jj)
     if (jj != g->j) wait_flag(my_flag(kind, rank_of(g->k, jj)), seq, s);
 }
@@ -1224,9 +1231,14 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   // barrier that orders this step's owner updates before the next step's peer pulls of the wire copies.
   TP_CUDA(cudaEventRecord(c.ev_ws1, c.ws));
   TP_CUDA(cudaEventRecord(c.ev_gs1, c.gs));
-  TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_ws1, 0));
-  TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_gs1, 0));
-  if (c.world > 1) TP_NCCL(ncclAllReduce(c.d_loss, c.d_loss, 1, ncclFloat64, ncclSum, c.world_comm, c.cs));
+  {
+    // the compute stream's tail: waiting for the last reductions / AdamW and the loss all-reduce (which also waits for
+    // the slowest rank) is exposed time of the step, accounted with the other exposed waits
+    Timed t(c.cs, 3, 0);
+    TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_ws1, 0));
+    TP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_gs1, 0));
+    if (c.world > 1) TP_NCCL(ncclAllReduce(c.d_loss, c.d_loss, 1, ncclFloat64, ncclSum, c.world_comm, c.cs));
+  }
   TP_CUDA(cudaMemcpyAsync(c.h_loss, c.d_loss, sizeof(double), cudaMemcpyDeviceToHost, c.cs));
   TP_CUDA(cudaEventRecord(c.ev_s1, c.cs));
   TP_CUDA(cudaStreamSynchronize(c.cs));

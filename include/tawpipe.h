@@ -34,7 +34,10 @@ extern "C" {
 
 #define TAWPIPE_OK          0
 #define TAWPIPE_ECONFIG    -2   /* invalid configuration / argument (SPEC.md:515 exit code 2)        */
-#define TAWPIPE_EINVARIANT -3   /* internal invariant failure (SPEC.md:515 exit code 3)              */
+#define TAWPIPE_EINVARIANT -3   /* internal invariant failure (SPEC.md:515 exit code 3): raised by the  *
+                                 * end-of-step check of the NVLink peer path when a sequence flag a peer *
+                                 * wrote does not end at the value the schedule implies (a lost,        *
+                                 * duplicated or mis-numbered signal)                                   */
 #define TAWPIPE_ERUNTIME   -4   /* CUDA or NCCL runtime error (SPEC.md:515 exit code 4)              */
 #define TAWPIPE_EUNINIT    -5   /* call before tawpipe_bootstrap / tawpipe_init                       */
 
@@ -157,6 +160,7 @@ int tawpipe_ledger(uint64_t* out, int n);
  *  [12] peak device bytes allocated (GB)             [13] wire bytes per element
  *  [14] elementwise/norm ms
  *  [15] algorithmic GFLOP of the recompute passes (checkpointing) executed in the step
+ *  [1] includes every compute-stream wait on peers and the step's tail (side-stream join + loss all-reduce)
  *  [16] 1 if the step ran the NVLink peer path (IPC-mapped copies / peer loads), 0 for NCCL collectives
  *  [17] GB of weight stripes this rank pulled over NVLink   [18] GB of gradients this rank's kernels read
  *       over NVLink (fp32 group stripes + wire-dtype rail partials)                                LOCAL. */

@@ -673,6 +673,13 @@ void adam_apply(const Unit& u, const GradSources& src, int n_src) {
 // Every cross-rank dependency is a sequence flag (RAW: "ready", WAR: "done reading"); the step-end loss all-reduce
 // orders one step's owner updates before the next step's pulls.
 inline int rank_of(int k, int j) { return k * g->G + j; }
+bool fault_gdone_plus1() {
+  static const bool on = [] {
+    const char* e = std::getenv("TAWPIPE_FAULT");
+    return e && std::string(e) == "gdone+1";
+  }();
+  return on;
+}
 inline uint32_t* flag_at(int dst_rank, int kind, int src_rank) {
   return static_cast<uint32_t*>(g->peer[dst_rank][PB_SIG]) + kind * kSigRanks + src_rank;
 }
@@ -808,7 +815,19 @@ void reduce_p2p(int uid, int slot, float* gacc) {
     }
     adam_apply(u, src, n);
     c.nvl_g_bytes += (4.0 * (c.G - 1) + static_cast<double>(c.esz) * (c.D - 1)) * u.s;
-    if (c.G > 1) signal_group(SK_GDONE, seq, s);
+    if (c.G > 1 && u.cls == U_E && c.j == 0 && fault_gdone_plus1()) {
+      // test-only fault (TAWPIPE_FAULT=gdone+1): member 0 mis-numbers its last GDONE of the step by one; waits are
+      // "≥", so nothing blocks -- exactly the silent class of protocol error the end-of-step check must catch
+      uint32_t* f[kMaxSignalTargets];
+      int nf = 0;
+      for (int jj = 1; jj < c.G; ++jj) {
+        f[nf++] = flag_at(rank_of(c.k, jj), SK_GDONE, c.rank);
+        expect_flag(SK_GDONE, rank_of(c.k, jj), seq);
+      }
+      signal_peers(f, nf, seq + 1, s);
+    } else if (c.G > 1) {
+      signal_group(SK_GDONE, seq, s);
+    }
     uint32_t* f[kMaxSignalTargets];
     int nf = 0;
     for (int kk = 0; kk < c.D; ++kk)

@@ -136,3 +136,19 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
         for i in range(P):
             for step in range(steps):
                 assert res[i]["comm_ms"][step] >= 0.95 * expect_ms, (i, step, res[i]["comm_ms"][step], expect_ms)
+
+
+def test_peer_flag_invariant_catches_a_misnumbered_signal(tmp_path):
+    """Race detector mutation test: with TAWPIPE_FAULT=gdone+1 member 0 of a 1×2 group over-numbers its last GDONE of
+    the step by one.  No wait blocks (waits are "≥"), so only the end-of-step flag check can see it: the step on
+    member 1 must fail with TAWPIPE_EINVARIANT naming the flag, instead of silently letting a later step run early."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
+           "--cfg", json.dumps(dict(C0B, n_layers=2)), "--G", "2", "--N", "2", "--steps", "1", "--dtype", "1",
+           "--out", str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, TAWPIPE_FAULT="gdone+1"))
+    out = r.stdout + r.stderr
+    assert r.returncode != 0 and "peer flag GDONE" in out and "error -3" in out, out[-3000:]

@@ -39,18 +39,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA/ALU pipes (offloads the MUFU unit, which is the softmax bottleneck at d_h = 128):
-// x = n + f with n = rint(x), f in [-0.5, 0.5]; 2^f by a degree-3 minimax polynomial (max rel. error 1.0e-4,
-// below bf16 rounding of P); 2^n added to the exponent field.  Valid for x in [-126, 0] (softmax arguments).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: rounds x to the nearest integer in the low mantissa bits
-  const float f = x - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.0550089308f, f, 0.242210984f), f, 0.69328293f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
-}
-// element k of a 32-wide chunk: emulate 3 of every 8 exponentials on the FMA pipe
-
 // packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2 / FMUL2: one issue slot for two lanes of work)
 __device__ __forceinline__ unsigned long long f2u(float2 a) {
   return (static_cast<unsigned long long>(__float_as_uint(a.y)) << 32) | __float_as_uint(a.x);
@@ -75,28 +63,8 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-// write one 128-element fp32 row as bf16 into a K-major SW128 tile pair (2 atoms of 64 columns)
-__device__ __forceinline__ void store_row_sw128(uint8_t* tile, int r, const float* v) {
-#pragma unroll
-  for (int a = 0; a < 2; ++a) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      uint4 o;
-      const float* x = v + a * 64 + c * 8;
-      o.x = pack_bf16(x[0], x[1]);
-      o.y = pack_bf16(x[2], x[3]);
-      o.z = pack_bf16(x[4], x[5]);
-      o.w = pack_bf16(x[6], x[7]);
-      *reinterpret_cast<uint4*>(tile + a * ATOM + r * 128 + ((c ^ (r & 7)) << 4)) = o;
-    }
-  }
-}
 
 // K-major SW128 descriptor for k-slice ks (16 elements) of a tile made of 64-column atoms
 __device__ __forceinline__ uint64_t desc_k(uint32_t base, int ks) {
@@ -786,7 +754,6 @@ __global__ void __launch_bounds__(384, 1)   // 352 threads; 168 registers (three
       mbar_wait(s_full, it & 1);
       if (t == 0) TR(it, 4);
       tc_fence_after();
-#pragma unroll
       // ls holds LSE·log2(e) (pre-scaled by the δ kernel); the diagonal tile (it == 0) takes the masked path
       uint32_t pk[4][16];   // Pᵀ_it, packed bf16, kept for the dS pass (Sᵀ_{it+1} overwrites its TMEM copy)
       auto p_pass = [&](auto diag) {

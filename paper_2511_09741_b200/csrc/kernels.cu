@@ -611,7 +611,7 @@ __global__ void rmsnorm_dgamma_v8_kernel(const bf16* __restrict__ dy, const bf16
 // loads), max and Σexp are block reductions over the registers, and dz is written once -- one read and one write
 // of the row (the three-pass ce_kernel re-read it twice)
 template <int NT, int NV>
-__global__ void __launch_bounds__(NT, 2) ce_v8_kernel(bf16* __restrict__ z, const int32_t* __restrict__ tgt, int V,
+__global__ void __launch_bounds__(NT) ce_v8_kernel(bf16* __restrict__ z, const int32_t* __restrict__ tgt, int V,
                                                    float inv_denom, float* __restrict__ loss_rows) {
   __shared__ float red[NT / 32];
   const int64_t row = blockIdx.x;
@@ -792,8 +792,8 @@ template <typename T>
 void cross_entropy(T* logits, const int32_t* targets, int64_t rows, int V, float inv_denom, float* loss_rows,
                    cudaStream_t s) {
   if constexpr (std::is_same<T, bf16>::value) {
-    if (V % 8 == 0 && V <= 8 * 256 * 16) {   // up to V = 32,768 in registers, 256 threads: 2 rows in flight per SM
-      ce_v8_kernel<256, 16><<<static_cast<unsigned>(rows), 256, 0, s>>>(logits, targets, V, inv_denom, loss_rows);
+    if (V % 8 == 0 && V <= 8 * 512 * 8) {   // up to V = 32,768 in registers
+      ce_v8_kernel<512, 8><<<static_cast<unsigned>(rows), 512, 0, s>>>(logits, targets, V, inv_denom, loss_rows);
       LAUNCHED();
       return;
     }

@@ -34,10 +34,11 @@ extern "C" {
 
 #define TAWPIPE_OK          0
 #define TAWPIPE_ECONFIG    -2   /* invalid configuration / argument (SPEC.md:515 exit code 2)        */
-#define TAWPIPE_EINVARIANT -3   /* internal invariant failure (SPEC.md:515 exit code 3): raised by the  *
-                                 * end-of-step check of the NVLink peer path when a sequence flag a peer *
-                                 * wrote does not end at the value the schedule implies (a lost,        *
-                                 * duplicated or mis-numbered signal)                                   */
+#define TAWPIPE_EINVARIANT -3   /* internal invariant failure (SPEC.md:515 exit code 3): a layer slot   *
+                                 * about to be computed on does not carry the version tag (unit, step)  *
+                                 * of that layer, or -- end-of-step check of the NVLink peer path -- a  *
+                                 * sequence flag a peer wrote does not end at the value the schedule    *
+                                 * implies (a lost, duplicated or mis-numbered signal)                  */
 #define TAWPIPE_ERUNTIME   -4   /* CUDA or NCCL runtime error (SPEC.md:515 exit code 4)              */
 #define TAWPIPE_EUNINIT    -5   /* call before tawpipe_bootstrap / tawpipe_init                       */
 

@@ -143,6 +143,7 @@ struct Ctx {
   uint32_t* sig = nullptr;                // this rank's flags [SK_*][source rank]
   void* part = nullptr;                   // rail partials of this rank's group (4 slots: layer 0/1, E, F) × max_s
   uint32_t wseq = 0, gseq = 0;            // gathers / reductions issued so far (identical on every rank)
+  int slot_tag[2][2] = {{-1, -1}, {-1, -1}};   // [slot] = {unit, step} of the last gather into it
   uint32_t wprev[2] = {0, 0}, gprev[2] = {0, 0}, pprev[4] = {0, 0, 0, 0};
   int pprev_owner[4] = {0, 0, 0, 0};      // the rank that read the previous partial in that slot
   double nvl_w_bytes = 0, nvl_g_bytes = 0;   // bytes this rank pulled / read over NVLink in the last step
@@ -430,8 +431,26 @@ void gather_p2p(int uid, int slot);
 void reduce_p2p(int uid, int slot, float* gacc);
 
 // a3: rail P2P of stripe j from the owner group (if remote) + intra-group all-gather, on ws
+// Version tags of the two layer slots (SURVEY §8(b) "version tag" invariant): the unit and step the last gather into
+// each slot was issued for; the compute checks them before reading a slot (host-side, every step).
+void tag_slot(int uid, int slot) {
+  if (g->units[uid].cls != U_BLOCK) return;
+  g->slot_tag[slot][0] = uid;
+  g->slot_tag[slot][1] = g->step_t;
+}
+void check_slot(int uid, int slot) {
+  const Unit& u = g->units[uid];
+  if (g->P == 1 || (g->G == 1 && u.owned)) return;   // the compute reads the owned wire copy, not a slot
+  if (g->slot_tag[slot][0] != uid || g->slot_tag[slot][1] != g->step_t)
+    throw Error(TAWPIPE_EINVARIANT, "layer slot " + std::to_string(slot) + " holds unit " +
+                                        std::to_string(g->slot_tag[slot][0]) + " of step " +
+                                        std::to_string(g->slot_tag[slot][1]) + ", compute needs layer " +
+                                        std::to_string(uid) + " of step " + std::to_string(g->step_t));
+}
+
 void gather(int uid, int slot) {
   const Unit& u = g->units[uid];
+  tag_slot(uid, slot);
   if (g->P == 1) return;  // nothing to move; the compute reads the owned copy in place
   if (g->p2p) {
     gather_p2p(uid, slot);
@@ -1191,6 +1210,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
       TP_CUDA(cudaEventRecord(c.evF, c.ws));
     }
     wait_on(c.cs, c.w_ready[slot]);
+    check_slot(l, slot);
     void* W = unit_buffer(l, slot);
     TRACE("forward layer %d\n", l);
     for (int mb = 0; mb < c.m; ++mb) layer_forward(l, mb, W, true);
@@ -1221,6 +1241,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
     wait_on(c.cs, c.g_free[slot]);
     if (c.p2p && c.gprev[slot]) wait_group_peers(SK_GDONE, c.gprev[slot], c.cs);   // peers done reading it
     TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.units[l].n_pad * 4, c.cs));
+    check_slot(l, slot);
     void* W = unit_buffer(l, slot);
     TRACE("backward layer %d\n", l);
     for (int mb = c.m - 1; mb >= 0; --mb) layer_backward(l, mb, W, c.gacc[slot]);  // last micro-batch first

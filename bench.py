@@ -331,7 +331,7 @@ def run_ours(args, c):
                 "exposed_ms": exposed,
                 "overlapped_ms": max(0.0, st["weight_comm_ms"] + g_ms - exposed)}
     else:
-        comm = {"path": "nccl",
+        comm = {"path": "nccl" if world > 1 else "none (P = 1: nothing gathered or reduced across GPUs)",
                 "weight_gather": {"ms": st["weight_comm_ms"], "bytes_recv": w_bytes,
                                   "gbs": w_bytes / max(st["weight_comm_ms"], 1e-9) / 1e6},
                 "grad_reduce": {"ms": st["grad_comm_ms"], "bytes_recv": g_bytes,

@@ -387,6 +387,8 @@ def run_ours(args, c):
         runs = [("fsdp_global_D1", world, T.GWPS), ("weipipe_ring", 1, T.RING)]
         if c["L"] % world == 0:   # NEXT-2: the paper-literal whole-layer owners with broadcast / reduce, same groups
             runs.append(("paper_literal_bcast_reduce", G, T.LITERAL))
+        if not args.no_cco:       # Table 4: TawPipe w/o CCO, same groups, prefetch serialised
+            runs.append(("tawpipe_wo_cco", G, T.NO_CCO))
         for name, Gb, sched in runs:
             T.bootstrap(rank, world, local, pg_backend="gloo")
             db = T.ModelDims(**{**dims.__dict__, "schedule": sched})
@@ -414,6 +416,8 @@ def run_ours(args, c):
                                       "exposed_comm_ms": bexp, "group_size": Gb, "steps": nb,
                                       "ledger_elems": sb.ledger()}
             sb.close()
+        # w/o GWPS = the group scheduler replaced by WeiPipe's ring exchange, i.e. weipipe_ring above
+        out["ablations"] = {"wo_gwps": "baselines.weipipe_ring", "wo_cco": "baselines.tawpipe_wo_cco"}
     if rank == 0:
         if not args.no_cpu_baseline:
             try:

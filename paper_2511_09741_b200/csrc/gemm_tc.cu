@@ -399,7 +399,7 @@ template <bool A_MN, bool B_MN, int EPI, int NSTAGE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     void* __restrict__ C, int64_t ldc, const bf16* __restrict__ R, int M, int N, int K,
-                    void* __restrict__ aux, int64_t ldx, int64_t I, int raster, RopeEpi rope) {
+                    void* __restrict__ aux, int64_t ldx, int64_t I, int raster, int l2hint, RopeEpi rope) {
   using Cfg = Gemm2Cfg<NSTAGE>;
   constexpr int BN = Cfg::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -440,6 +440,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 
   if (warp == 4) {
     if (lane == 0) {
+      // l2hint & 3 = 1: the raster keeps an A band resident, 2: a B band -- that operand is loaded evict_last, the
+      // streamed one evict_first (l2hint & 4) or evict_normal; 0: evict_normal for both (long-K wgrads)
+      const uint64_t last = l2_policy_evict_last(), normal = l2_policy_evict_normal();
+      const uint64_t stream = (l2hint & 4) ? l2_policy_evict_first() : normal;
+      const uint64_t pol_a = (l2hint & 3) == 1 ? last : (l2hint & 3) ? stream : normal;
+      const uint64_t pol_b = (l2hint & 3) == 2 ? last : (l2hint & 3) ? stream : normal;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cl; t < num_tiles; t += n_cl) {
@@ -455,16 +461,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
           const uint32_t bar = mapa_shared(&full[stage], 0);
           if (!A_MN) {
-            tma_load_2d_cg2(sa, &tmA, bar, kb * BK, m0);
+            tma_load_2d_cg2_hint(sa, &tmA, bar, kb * BK, m0, pol_a);
           } else {
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i) tma_load_2d_cg2(sa + i * 8192, &tmA, bar, m0 + i * 64, kb * BK);
+            for (int i = 0; i < BM / 64; ++i) tma_load_2d_cg2_hint(sa + i * 8192, &tmA, bar, m0 + i * 64, kb * BK, pol_a);
           }
           if (!B_MN) {
-            tma_load_2d_cg2(sb, &tmB, bar, kb * BK, n0);
+            tma_load_2d_cg2_hint(sb, &tmB, bar, kb * BK, n0, pol_b);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 128; ++i) tma_load_2d_cg2(sb + i * 8192, &tmB, bar, n0 + i * 64, kb * BK);
+            for (int i = 0; i < BN / 128; ++i)
+              tma_load_2d_cg2_hint(sb + i * 8192, &tmB, bar, n0 + i * 64, kb * BK, pol_b);
           }
           if (++stage == Cfg::STAGES) {
             stage = 0;
@@ -593,7 +600,16 @@ int g_num_sms = 0;
 // the orientation with the fewer estimated HBM operand reads.  Long-K GEMMs (the wgrads, K = tokens) stream K in
 // lockstep across the in-flight tiles, so their reuse is per K slice and the default M-band order is kept.
 // TAWPIPE_GEMM_RASTER=m|n|default forces an orientation (experiments).
-int choose_raster(int64_t num_m, int64_t num_n, int64_t rows_m, int64_t rows_n, int64_t K, int default_group) {
+int choose_raster(int64_t num_m, int64_t num_n, int64_t rows_m, int64_t rows_n, int64_t K, int default_group,
+                  int* l2hint = nullptr) {
+  // l2hint (CTA-pair GEMM): which operand's band the raster keeps resident -- 1 A, 2 B, 0 none (default order),
+  // + 4: the streamed operand evict_first.  TAWPIPE_GEMM_L2HINT = 0 (none), 1 (resident evict_last), 2 (+ streamed
+  // evict_first) -- experiments
+  static const int hints = [] {
+    const char* e = std::getenv("TAWPIPE_GEMM_L2HINT");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (l2hint) *l2hint = 0;
   static const int force = [] {
     const char* e = std::getenv("TAWPIPE_GEMM_RASTER");
     if (!e) return 0;
@@ -613,6 +629,7 @@ int choose_raster(int64_t num_m, int64_t num_n, int64_t rows_m, int64_t rows_n, 
   const int64_t reads_m = a_bytes + b_bytes * ((num_m + gm - 1) / gm);
   const int64_t reads_n = b_bytes + a_bytes * ((num_n + gn - 1) / gn);
   const bool use_n = force == 2 || (force == 0 && reads_n < reads_m);
+  if (l2hint && hints) *l2hint = (use_n ? 2 : 1) | (hints >= 2 ? 4 : 0);
   return use_n ? -static_cast<int>(gn) : static_cast<int>(gm);
 }
 
@@ -706,9 +723,11 @@ void launch2_n(const GemmArgs& g, cudaStream_t s) {
   CUtensorMap tb = B_MN ? make_tmap_bf16_2d(g.B, g.N, g.K, g.ldb, 64) : make_tmap_bf16_2d(g.B, g.K, g.N, g.ldb, Cfg::BN / 2);
   const int tiles = static_cast<int>((g.M / (2 * BM)) * (g.N / Cfg::BN));
   const int grid = 2 * (tiles < clusters_fit ? tiles : clusters_fit);
-  const int raster = choose_raster(g.M / (2 * BM), g.N / Cfg::BN, 2 * BM, Cfg::BN, g.K, 8);
+  int l2hint = 0;
+  const int raster = choose_raster(g.M / (2 * BM), g.N / Cfg::BN, 2 * BM, Cfg::BN, g.K, 8, &l2hint);
   kern<<<grid, 192, Cfg::SMEM, s>>>(ta, tb, g.C, g.ldc, static_cast<const bf16*>(g.R), static_cast<int>(g.M),
-                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster, g.rope);
+                                     static_cast<int>(g.N), static_cast<int>(g.K), g.aux, g.ldx, g.I, raster, l2hint,
+                                     g.rope);
   TP_CUDA(cudaGetLastError());
   g_kstats.launches++;
 }

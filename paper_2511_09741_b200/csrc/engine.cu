@@ -991,8 +991,20 @@ void layer_forward(int l, int mb, void* W, bool write_out) {
   if (!write_out) g->recompute_gflop += work * 1e-9;
 }
 
-void layer_backward(int l, int mb, void* W, float* G_) {
+// Gradient accumulators are not zeroed by a full memset per layer: the first micro-batch's wgrad GEMMs store
+// (EPI_F32_STORE) and the later ones accumulate; only the two RMSNorm-gain ranges (atomic partial sums) are zeroed
+// (gacc_store_first).  0 + x == x in fp32, so the values are identical to memset + accumulate.
+bool gacc_store_first() {
+  static const bool on = [] {
+    const char* e = std::getenv("TAWPIPE_GACC_ZERO");
+    return !(e && std::string(e) == "memset");
+  }();
+  return on;
+}
+
+void layer_backward(int l, int mb, void* W, float* G_, bool first) {
   cudaStream_t s = g->cs;
+  const bool acc = !(first && gacc_store_first());
   const int64_t T = g->T, H = g->H, I = g->I;
   LayerW w = layer_weights(W);
   // recompute from the checkpoint h_l; the last layer's last micro-batch is still resident in the
@@ -1007,7 +1019,7 @@ void layer_backward(int l, int mb, void* W, float* G_) {
   float* ggu = G_ + 2 * H + 4 * H * H;     // Wgate|Wup [2I, H]
   float* gd = G_ + 2 * H + 4 * H * H + 2 * I * H;  // Wdown [H, I]
   // h2 = h1 + y·Wdownᵀ
-  gemm(H, I, T, dh, H, false, A.y, I, false, gd, I, true, true, nullptr, s);
+  gemm(H, I, T, dh, H, false, A.y, I, false, gd, I, true, acc, nullptr, s);
   if (g->bf && !gemm_force_simt()) {
     // dgrad of the down projection with the SwiGLU backward in the epilogue: dY never reaches HBM
     GemmArgs a{T, I, H, dh, H, true, w.wdown, I, false, g->dGU, 2 * I, false, false, nullptr};
@@ -1023,15 +1035,15 @@ void layer_backward(int l, int mb, void* W, float* G_) {
     BY_TYPE(swiglu_bwd<float>((const float*)g->dY, (const float*)A.gu, (float*)g->dGU, T, (int)I, s),
             swiglu_bwd<bf16>((const bf16*)g->dY, (const bf16*)A.gu, (bf16*)g->dGU, T, (int)I, s));
   }
-  gemm(2 * I, H, T, g->dGU, 2 * I, false, A.b, H, false, ggu, H, true, true, nullptr, s);
+  gemm(2 * I, H, T, g->dGU, 2 * I, false, A.b, H, false, ggu, H, true, acc, nullptr, s);
   gemm(T, H, 2 * I, g->dGU, 2 * I, true, w.wgu, H, false, g->db, H, false, false, nullptr, s);
   k_rmsnorm_bwd(g->db, A.h1, w.mlp_norm, A.r2, dh, g->dh1, gmn, T, s);
   // h1 = h + o·Woᵀ
-  gemm(H, H, T, g->dh1, H, false, A.o, H, false, go, H, true, true, nullptr, s);
+  gemm(H, H, T, g->dh1, H, false, A.o, H, false, go, H, true, acc, nullptr, s);
   gemm(T, H, H, g->dh1, H, true, w.wo, H, false, g->dO, H, false, false, nullptr, s);
   attn_bwd(A.qkv, A.o, A.lse, g->dO, g->dqkv, s);
   if (!use_tc_attention()) k_rope(g->dqkv, true, s);   // the tcgen05 backward applies it in its epilogues
-  gemm(3 * H, H, T, g->dqkv, 3 * H, false, A.a, H, false, gq, H, true, true, nullptr, s);
+  gemm(3 * H, H, T, g->dqkv, 3 * H, false, A.a, H, false, gq, H, true, acc, nullptr, s);
   gemm(T, H, 3 * H, g->dqkv, 3 * H, true, w.wqkv, H, false, g->da, H, false, false, nullptr, s);
   k_rmsnorm_bwd(g->da, hin, w.attn_norm, A.r1, g->dh1, dh, G_, T, s);
 }
@@ -1055,7 +1067,8 @@ void head(int mb, void* F, float* GF) {
       BY_TYPE(cross_entropy<float>((float*)g->logits, tg, tc, (int)V, inv_denom, g->loss_rows + c0, s),
               cross_entropy<bf16>((bf16*)g->logits, tg, tc, (int)V, inv_denom, g->loss_rows + c0, s));
     }
-    gemm(V, H, tc, g->logits, V, false, fc, H, false, GF + H, H, true, true, nullptr, s);
+    const bool acc = !(mb == 0 && c0 == 0 && gacc_store_first());   // the first chunk stores (see layer_backward)
+    gemm(V, H, tc, g->logits, V, false, fc, H, false, GF + H, H, true, acc, nullptr, s);
     gemm(tc, H, V, g->logits, V, true, Wh, H, false, wptr(g->df, c0 * H), H, false, false, nullptr, s);
   }
   k_rmsnorm_bwd(g->df, hL, gf, g->rstd_f, nullptr, g->dhb[mb], GF, T, s);
@@ -1223,7 +1236,10 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   }
   // ---- head F (a6)
   wait_on(c.cs, c.evF);
-  TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.units[F].n_pad * 4, c.cs));
+  if (gacc_store_first())
+    TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.H * 4, c.cs));   // final-norm gain (atomic partial sums)
+  else
+    TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.units[F].n_pad * 4, c.cs));
   void* Fbuf = unit_buffer(F, 0);
   for (int mb = 0; mb < c.m; ++mb) head(mb, Fbuf, c.gaccF);
   TP_CUDA(cudaEventRecord(c.evGF, c.cs));
@@ -1240,11 +1256,16 @@ double run_step(const int32_t* tokens, bool device_tokens) {
     if (l != c.L - 1) wait_on(c.cs, c.w_ready[slot]);  // r = 1: layer L-1 reuses its forward buffer (R12)
     wait_on(c.cs, c.g_free[slot]);
     if (c.p2p && c.gprev[slot]) wait_group_peers(SK_GDONE, c.gprev[slot], c.cs);   // peers done reading it
-    TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.units[l].n_pad * 4, c.cs));
+    if (gacc_store_first()) {   // the two norm gains; the weight matrices are stored by the first micro-batch
+      TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.H * 4, c.cs));
+      TP_CUDA(cudaMemsetAsync(c.gacc[slot] + c.H + 4 * static_cast<int64_t>(c.H) * c.H, 0, c.H * 4, c.cs));
+    } else {
+      TP_CUDA(cudaMemsetAsync(c.gacc[slot], 0, c.units[l].n_pad * 4, c.cs));
+    }
     check_slot(l, slot);
     void* W = unit_buffer(l, slot);
     TRACE("backward layer %d\n", l);
-    for (int mb = c.m - 1; mb >= 0; --mb) layer_backward(l, mb, W, c.gacc[slot]);  // last micro-batch first
+    for (int mb = c.m - 1; mb >= 0; --mb) layer_backward(l, mb, W, c.gacc[slot], mb == c.m - 1);  // last first
     TP_CUDA(cudaEventRecord(c.w_free[slot], c.cs));
     TP_CUDA(cudaEventRecord(c.g_ready[slot], c.cs));
     if (!cco && l - 1 >= 0) {
@@ -1531,6 +1552,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   c.gaccF = (float*)dmalloc(c.units[L + 1].n_pad * 4);
   TP_CUDA(cudaMemsetAsync(c.gacc[0], 0, c.units[0].n_pad * 4, c.cs));
   TP_CUDA(cudaMemsetAsync(c.gacc[1], 0, c.units[0].n_pad * 4, c.cs));
+  TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.units[L + 1].n_pad * 4, c.cs));   // padding stays zero (nothing writes it)
   if (G > 1 || D > 1) c.gwire = dmalloc(c.max_pad * esz);
   if (G > 1) c.rsout = dmalloc(c.max_s * esz);
   if (D > 1) c.crecv = dmalloc(c.max_s * (D - 1) * esz);

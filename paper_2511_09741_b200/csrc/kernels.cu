@@ -841,8 +841,16 @@ void adamw_grouped(const GradSources& src, float* master, float* m, float* v, W*
              reinterpret_cast<uintptr_t>(v) % 32 == 0 && reinterpret_cast<uintptr_t>(wire) % 16 == 0;
   for (int si = 0; si < src.group_end[src.n_groups - 1]; ++si)
     vec = vec && reinterpret_cast<uintptr_t>(src.p[si]) % ((src.f32_mask >> si & 1u) ? 32 : 16) == 0;
+  // TAWPIPE_ADAM_GRID=k caps the grid at k blocks (experiments: a small grid co-resides with the compute stream's
+  // GEMM CTAs and runs in the background instead of taking every SM for ≈1 ms per layer)
+  static const unsigned adam_grid = [] {
+    const char* e = std::getenv("TAWPIPE_ADAM_GRID");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 0u;
+  }();
+  unsigned blocks = grid_stride_blocks(n / 8);
+  if (adam_grid > 0 && blocks > adam_grid) blocks = adam_grid;
   if (vec)
-    adamw_grouped_v8_kernel<W><<<grid_stride_blocks(n / 8), 256, 0, s>>>(src, master, m, v, wire, n, unit_off, nd, p);
+    adamw_grouped_v8_kernel<W><<<blocks, 256, 0, s>>>(src, master, m, v, wire, n, unit_off, nd, p);
   else
     adamw_grouped_kernel<W><<<grid_stride_blocks(n), 256, 0, s>>>(src, master, m, v, wire, n, unit_off, nd, p);
   LAUNCHED();

@@ -569,265 +569,6 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-// ----------------------------------------------------------------------------------------------- forward v8
-// fa_fwd7 on CTA pairs (cluster of 2, tcgen05 cta_group::2), d_h = 128.  Each CTA keeps fa_fwd7's two query tiles and
-// softmax warpgroups; the pair's MMAs are M = 256 (tile A of both CTAs, then tile B of both), issued by the leader
-// CTA.  The B operands are split between the pair: for S = Q·Kᵀ each CTA stages 32 of every 64-key half of K, for
-// O += P·V its 64 of the 128 V columns -- so each CTA's shared memory receives and feeds the tensor core half the
-// K / V bytes of fa_fwd7 (shared-memory traffic per 128 keys: 160 KB instead of 256 KB, DESIGN.md §5 ceilings).
-// Query tiles per cluster u: rank 0 {A = 4u+3, B = 4u}, rank 1 {A = 4u+2, B = 4u+1}; the tile-A stream runs 4u+4
-// key tiles, the tile-B stream 4u+2, and a CTA whose own tile needs one key tile fewer sees it fully masked.
-//   TMEM per CTA as fa_fwd7 (S/P [128t, 128t+128), O_t [256+128t, 384+128t)), allocated by the pair.
-struct Fwd8Smem {
-  static constexpr int QB = 2 * ATOM;        // one 128-row query tile (2 atoms of 64 columns)
-  static constexpr int NST = 4;               // K / V stages
-  static constexpr int KB = 2 * 8192;         // this CTA's K share of a 128-key stage: 2 atoms × 64 rows
-  static constexpr int VB = ATOM;             // this CTA's V share: one 128-row atom (64 columns)
-  static constexpr int OFF_Q = 0;             // Q_A, Q_B
-  static constexpr int OFF_K = 2 * QB;
-  static constexpr int OFF_V = OFF_K + NST * KB;
-  static constexpr int OFF_BAR = OFF_V + NST * VB;
-  static constexpr int BYTES = OFF_BAR + 256;
-};
-// K-major descriptor over atoms of `atom` bytes (64 columns each)
-__device__ __forceinline__ uint64_t desc_k_atom(uint32_t base, int ks, int atom) {
-  return umma_desc_sw128(base + (ks >> 2) * atom + (ks & 3) * 32, 16, 1024);
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
-    fa_fwd8_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm32,
-                   bf16* __restrict__ out, float* __restrict__ lse, int S, int nh, float scale2) {
-  constexpr int DH = 128;
-  using L = Fwd8Smem;
-  constexpr int NST = L::NST;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 1 + NST, *v_full = bar + 1 + 2 * NST,
-           *v_empty = bar + 1 + 3 * NST;
-  uint64_t* s_full = bar + 1 + 4 * NST;    // [tile][half]
-  uint64_t* p_ready = bar + 5 + 4 * NST;   // [tile][half], leader's copy counts both CTAs' softmax warps
-  uint64_t* o_done = bar + 9 + 4 * NST;    // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 11 + 4 * NST);
-
-  const uint32_t rank = cluster_ctarank();
-  const int n_u = S / BQ / 4;
-  const int cl = static_cast<int>(blockIdx.x >> 1);
-  const int u = n_u - 1 - cl % n_u;   // heaviest clusters first
-  const int h = cl / n_u;
-  const int b = blockIdx.y;
-  const int H = nh * DH;
-  const int row0 = b * S;
-  const int n_kv_A = 4 * u + 4;        // key tiles of the tile-A stream (the whole K / V stream)
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-  if (threadIdx.x == 0) {
-    if (smem_u32(sm) & 1023) __trap();
-    tma_prefetch(&tm);
-    tma_prefetch(&tm32);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 2);   // released by both tiles' issuers
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 2);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_ready[i], 8);   // one arrival per softmax warp of the tile, both CTAs (leader's copy used)
-    }
-    mbar_init(&o_done[0], 1);
-    mbar_init(&o_done[1], 1);
-    fence_mbar_init();
-  }
-  if (warp == 8) tmem_alloc_cg2(tmem_slot, 512);   // warps 0-7 softmax, 8 / 10 issuers (leader), 9 producer
-  tc_fence_before();
-  cluster_sync();   // both CTAs' barriers initialised and TMEM allocated before any cross-CTA traffic
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 9) {
-    if (lane == 0) {
-      // this CTA's query tiles and its share of every K / V tile; completion counted on the leader's barriers
-      if (rank == 0) mbar_expect_tx(q_full, 2 * 2 * L::QB);
-      const uint32_t qb = mapa_shared(q_full, 0);
-      const int qa = 4 * u + 3 - static_cast<int>(rank), qbt = 4 * u + static_cast<int>(rank);
-      for (int t = 0; t < 2; ++t)
-        for (int a = 0; a < 2; ++a)
-          tma_load_2d_cg2(sm + L::OFF_Q + t * L::QB + a * ATOM, &tm, qb, h * DH + a * 64, row0 + (t ? qbt : qa) * BQ);
-      for (int j = 0; j < n_kv_A; ++j) {
-        const int st = j % NST;
-        const uint32_t ph = (j / NST) & 1;
-        mbar_wait_sleep(&k_empty[st], ph ^ 1);
-        if (rank == 0) mbar_expect_tx(&k_full[st], 2 * L::KB);
-        const uint32_t kb = mapa_shared(&k_full[st], 0);
-        for (int hf = 0; hf < 2; ++hf)     // keys 64·hf + 32·rank .. +31 of the tile -> rows 32·hf .. of each atom
-          for (int a = 0; a < 2; ++a)
-            tma_load_2d_cg2(sm + L::OFF_K + st * L::KB + a * 8192 + hf * 4096, &tm32, kb, H + h * DH + a * 64,
-                            row0 + j * BQ + hf * 64 + static_cast<int>(rank) * 32);
-        mbar_wait_sleep(&v_empty[st], ph ^ 1);
-        if (rank == 0) mbar_expect_tx(&v_full[st], 2 * L::VB);
-        tma_load_2d_cg2(sm + L::OFF_V + st * L::VB, &tm, mapa_shared(&v_full[st], 0),
-                        2 * H + h * DH + static_cast<int>(rank) * 64, row0 + j * BQ);
-      }
-    }
-  } else if (warp == 8 || warp == 10) {
-    if (rank == 0) {
-      const int t = warp == 8 ? 0 : 1;
-      const int n_kv_t = n_kv_A - 2 * t;
-      const int last_rel = n_kv_A - 1 - NST;   // stages of later tiles are never refilled: no release needed
-      constexpr uint32_t id_qk = umma_idesc_bf16(256, 64, false, false);
-      constexpr uint32_t id_pv = umma_idesc_bf16(256, DH, false, true);
-      const uint32_t sQ = smem_u32(sm + L::OFF_Q + t * L::QB);
-      auto issue_s = [&](int jj, int hf) {   // S_t(jj, hf) = Q_t · K_jj[64·hf ..]ᵀ, N = 64 (32 keys per CTA)
-        const uint32_t sK = smem_u32(sm + L::OFF_K + (jj % NST) * L::KB) + hf * 4096;
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_f16_cg2_w(tmem + t * 128 + hf * 64, desc_k(sQ, ks), desc_k_atom(sK, ks, 8192), id_qk, ks > 0);
-        umma_commit_cg2_w(&s_full[t * 2 + hf], 0x3);
-      };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(0, 1);
-      if (0 <= last_rel) umma_commit_cg2_w(&k_empty[0], 0x3);
-      for (int j = 0; j < n_kv_t; ++j) {
-        const int st = j % NST;
-        mbar_wait(&v_full[st], (j / NST) & 1);
-        const uint32_t sV = smem_u32(sm + L::OFF_V + st * L::VB);
-        const bool next = j + 1 < n_kv_t;
-        if (next) mbar_wait(&k_full[(j + 1) % NST], ((j + 1) / NST) & 1);
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          mbar_wait_cluster(&p_ready[t * 2 + hf], j & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            umma_f16_tmemA_cg2_w(tmem + 256 + t * 128, tmem + t * 128 + hf * 64 + ks * 8, desc_mn(sV, hf * 4 + ks),
-                                 id_pv, (j | hf | ks) > 0);
-          umma_commit_cg2_w(&o_done[t], 0x3);
-          if (next) issue_s(j + 1, hf);
-        }
-        if (j <= last_rel) umma_commit_cg2_w(&v_empty[st], 0x3);
-        if (next && j + 1 <= last_rel) umma_commit_cg2_w(&k_empty[(j + 1) % NST], 0x3);
-      }
-    }
-  } else {
-    const int t = warp >> 2;          // 0: tile A, 1: tile B
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const int qt = t == 0 ? 4 * u + 3 - static_cast<int>(rank) : 4 * u + static_cast<int>(rank);
-    const int n_kv = n_kv_A - 2 * t;  // the stream's key tiles: this CTA's last one may be fully masked
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
-    const uint32_t p_ready_leader = mapa_shared(&p_ready[0], 0);
-    float m2 = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kv; ++j) {
-#pragma unroll 1
-      for (int hf = 0; hf < 2; ++hf) {
-        const uint32_t tS = tmem + t * 128 + hf * 64 + lane_off;
-        mbar_wait(&s_full[t * 2 + hf], j & 1);
-        tc_fence_after();
-        float s[64];
-        {
-          uint32_t u0[32], u1[32];
-          tmem_ld32(tS, u0);
-          tmem_ld32(tS + 32, u1);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            s[i] = __uint_as_float(u0[i]);
-            s[32 + i] = __uint_as_float(u1[i]);
-          }
-        }
-        if (j >= qt) {  // the diagonal tile (and, one past it, a fully masked one): key > row is masked
-          const int off = (j - qt) * BQ + hf * 64;
-#pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (off + i > r) s[i] = -INFINITY;
-        }
-        float mxa[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) mxa[k] = s[k];
-#pragma unroll
-        for (int i = 8; i < 64; ++i) mxa[i & 7] = fmaxf(mxa[i & 7], s[i]);
-        float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                         fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
-        mx *= scale2;
-        if (j == 0 && hf == 0) {
-          m2 = mx;
-        } else if (__any_sync(0xffffffffu, mx > m2 + 8.0f)) {
-          mbar_wait(&o_done[t], (2 * j + hf - 1) & 1);
-          tc_fence_after();
-          const float mnew = fmaxf(m2, mx);
-          const float alpha = ex2(m2 - mnew);
-          l *= alpha;
-#pragma unroll 1
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t uu[32];
-            tmem_ld32(tO + c * 32, uu);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) uu[i] = __float_as_uint(__uint_as_float(uu[i]) * alpha);
-            tmem_st32(tO + c * 32, uu);
-          }
-          m2 = mnew;
-        }
-        float2 sa2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        const float2 sc2 = make_float2(scale2, scale2), nm2 = make_float2(-m2, -m2);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pw[16];
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float2 a2 = ffma2(make_float2(s[c * 32 + i], s[c * 32 + i + 1]), sc2, nm2);
-            const float p0 = ex2(a2.x), p1 = ex2(a2.y);
-            sa2[(i >> 1) & 3] = fadd2(sa2[(i >> 1) & 3], make_float2(p0, p1));
-            pw[i / 2] = pack_bf16(p0, p1);
-          }
-          tmem_st16(tS + c * 16, pw);
-        }
-        const float2 t2 = fadd2(fadd2(sa2[0], sa2[1]), fadd2(sa2[2], sa2[3]));
-        l += t2.x + t2.y;
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(p_ready_leader + (t * 2 + hf) * 8);
-      }
-    }
-    mbar_wait(&o_done[t], 0);
-    mbar_wait(&o_done[t], 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    bf16* orow = out + static_cast<int64_t>(row0 + qt * BQ + r) * H + h * DH;
-#pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t uu[32];
-      tmem_ld32(tO + c * 32, uu);
-      tmem_wait_ld();
-      uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        uint4 o;
-        o.x = pack_bf16(__uint_as_float(uu[8 * v + 0]) * inv, __uint_as_float(uu[8 * v + 1]) * inv);
-        o.y = pack_bf16(__uint_as_float(uu[8 * v + 2]) * inv, __uint_as_float(uu[8 * v + 3]) * inv);
-        o.z = pack_bf16(__uint_as_float(uu[8 * v + 4]) * inv, __uint_as_float(uu[8 * v + 5]) * inv);
-        o.w = pack_bf16(__uint_as_float(uu[8 * v + 6]) * inv, __uint_as_float(uu[8 * v + 7]) * inv);
-        d4[v] = o;
-      }
-    }
-    lse[(static_cast<int64_t>(b) * nh + h) * S + qt * BQ + r] = (m2 + __log2f(l)) * (1.0f / LOG2E);
-    tc_fence_before();
-  }
-  __syncthreads();
-  cluster_sync();   // the peer's TMEM / barriers stay alive until the leader's last MMA and commit have landed
-  if (warp == 8) {
-    tc_fence_after();
-    tmem_dealloc_cg2(tmem, 512);
-  }
-}
-
 // =============================================================================================== backward
 // Warp roles (320 threads, one CTA per SM):
 //   warps 0-3  softmax-gradient warps, thread t <-> key row t of the tile (TMEM lane t):
@@ -1350,17 +1091,7 @@ void attention_fwd_tc(int B, int S, int nh, int dh, const bf16* qkv, bf16* o, fl
   const int H = nh * dh;
   CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ll * H, static_cast<int64_t>(B) * S, 3ll * H, 128);
   const float scale2 = LOG2E / sqrtf(static_cast<float>(dh));
-  // TAWPIPE_FA_FWD=8 selects the CTA-pair forward (d_h = 128, query tiles a multiple of 4), 7 the single-CTA one
-  static const int fwd_ver = [] {
-    const char* e = std::getenv("TAWPIPE_FA_FWD");
-    return e ? std::atoi(e) : 7;
-  }();
-  if (fwd_ver == 8 && dh == 128 && (S / BQ) % 4 == 0) {
-    CUtensorMap tm32 = make_tmap_bf16_2d(qkv, 3ll * H, static_cast<int64_t>(B) * S, 3ll * H, 32);
-    dim3 grid8(static_cast<unsigned>(2 * (S / BQ / 4) * nh), static_cast<unsigned>(B));
-    prep(fa_fwd8_kernel, Fwd8Smem::BYTES);
-    fa_fwd8_kernel<<<grid8, 352, Fwd8Smem::BYTES, s>>>(tm, tm32, o, lse, S, nh, scale2);
-  } else if ((S / BQ) % 2 == 0) {
+  if ((S / BQ) % 2 == 0) {
     dim3 grid7(static_cast<unsigned>((S / BQ / 2) * nh), static_cast<unsigned>(B));
     if (dh == 128) {
       prep(fa_fwd7_kernel<128>, Fwd5Smem<128>::BYTES);

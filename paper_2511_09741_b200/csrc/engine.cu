@@ -135,6 +135,7 @@ struct Ctx {
   double* d_loss = nullptr;
   double* h_loss = nullptr;
   uint64_t ledger[TAWPIPE_LEDGER_N] = {};
+  uint64_t ledger_plan[TAWPIPE_LEDGER_N] = {};   // what the documented schedule moves per step (plan_ledger)
   int step_t = 0;
   // NVLink peer path of the GWPS schedule (peer.cu): IPC-mapped buffers of every rank, sequence flags
   bool p2p = false;
@@ -1305,6 +1306,10 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   TP_CUDA(cudaStreamSynchronize(c.cs));
   TP_CUDA(cudaDeviceSynchronize());
   if (c.p2p) check_flags();
+  for (int i = 0; i < TAWPIPE_LEDGER_N; ++i)   // the executed transfers are the planned schedule's, counter by counter
+    TP_CHECK(c.ledger[i] == c.ledger_plan[i], TAWPIPE_EINVARIANT,
+             "step ledger counter " + std::to_string(i) + " is " + std::to_string(c.ledger[i]) + ", the plan's " +
+                 std::to_string(c.ledger_plan[i]));
   // ---- stats
   std::memset(c.stats, 0, sizeof(c.stats));
   float ms = 0.f;
@@ -1379,6 +1384,34 @@ struct Plan {
   std::vector<Unit> units;
   int64_t owned_total = 0, max_pad = 0, max_s = 0;
 };
+// The per-step ledger of the documented schedule, written out as its own sequence (not by replaying run_step): E
+// gather, forward gathers 0..L-1, F gather, F reduction, backward gathers L-2..0 (layer L-1 reuses its forward
+// buffer, R12) with reductions L-1..0, E reduction.  tawpipe_plan returns it; every step checks its executed ledger
+// against it (TAWPIPE_EINVARIANT), so a schedule change that skips or repeats a transfer fails loudly.
+void plan_ledger(const Plan& pl, int P, int G, int L, int schedule, int rank, uint64_t* led) {
+  const int D = P / G;
+  const bool ring = (schedule & TAWPIPE_RING) != 0, literal = (schedule & TAWPIPE_LITERAL) != 0;
+  auto gat = [&](const Unit& u) {
+    if (ring) ledger_gather_ring(u, rank, P, led);
+    else if (literal) ledger_gather_literal(u, G, D, rank / G, rank % G, led);
+    else ledger_gather(u, G, D, led);
+  };
+  auto red = [&](const Unit& u) {
+    if (ring) ledger_reduce_ring(u, rank, P, led);
+    else if (literal) ledger_reduce_literal(u, G, D, rank / G, rank % G, led);
+    else ledger_reduce(u, G, D, led);
+  };
+  gat(pl.units[L]);
+  for (int l = 0; l < L; ++l) gat(pl.units[l]);
+  gat(pl.units[L + 1]);
+  red(pl.units[L + 1]);
+  for (int l = L - 1; l >= 0; --l) {
+    if (l != L - 1) gat(pl.units[l]);
+    red(pl.units[l]);
+  }
+  red(pl.units[L]);
+}
+
 Plan make_plan(int P, int G, int L, int64_t H, int64_t I, int64_t V, int rank, bool literal) {
   Plan pl;
   const int D = P / G, k = rank / G, j = rank % G;
@@ -1496,6 +1529,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   c.phi = 4 * H * H + 3 * H * I + 2 * H;
   {
     Plan pl = make_plan(P, G, L, H, I, V, c.rank, (d->schedule & TAWPIPE_LITERAL) != 0);
+    plan_ledger(pl, P, G, L, d->schedule, c.rank, c.ledger_plan);
     c.units = pl.units;
     c.owned_total = pl.owned_total;
     c.max_pad = pl.max_pad;
@@ -1757,33 +1791,10 @@ int tawpipe_plan(int n_devices, int group_size, int n_layers, const tawpipe_dims
   return guarded([&] {
     validate(n_devices, group_size, n_layers, dims, n_micro, n_devices);
     TP_CHECK(rank >= 0 && rank < n_devices, TAWPIPE_ECONFIG, "rank out of range");
-    const int G = group_size, D = n_devices / group_size, L = n_layers;
     const bool literal = (dims->schedule & TAWPIPE_LITERAL) != 0;
-    Plan pl = make_plan(n_devices, G, L, dims->hidden, dims->ffn, dims->vocab, rank, literal);
+    Plan pl = make_plan(n_devices, group_size, n_layers, dims->hidden, dims->ffn, dims->vocab, rank, literal);
     uint64_t led[TAWPIPE_LEDGER_N] = {};
-    const bool ring = (dims->schedule & TAWPIPE_RING) != 0;
-    const int P = n_devices;
-    auto gat = [&](const Unit& u) {
-      if (ring) ledger_gather_ring(u, rank, P, led);
-      else if (literal) ledger_gather_literal(u, G, D, rank / G, rank % G, led);
-      else ledger_gather(u, G, D, led);
-    };
-    auto red = [&](const Unit& u) {
-      if (ring) ledger_reduce_ring(u, rank, P, led);
-      else if (literal) ledger_reduce_literal(u, G, D, rank / G, rank % G, led);
-      else ledger_reduce(u, G, D, led);
-    };
-    // the step's communication sequence (run_step): E gather, forward gathers 0..L-1, F gather, F reduction,
-    // backward gathers L-2..0 (layer L-1 reuses its forward buffer, R12) with reductions L-1..0, E reduction
-    gat(pl.units[L]);
-    for (int l = 0; l < L; ++l) gat(pl.units[l]);
-    gat(pl.units[L + 1]);
-    red(pl.units[L + 1]);
-    for (int l = L - 1; l >= 0; --l) {
-      if (l != L - 1) gat(pl.units[l]);
-      red(pl.units[l]);
-    }
-    red(pl.units[L]);
+    plan_ledger(pl, n_devices, group_size, n_layers, dims->schedule, rank, led);
     if (ledger_out) std::memcpy(ledger_out, led, sizeof(led));
     if (shard_elems_out) *shard_elems_out = pl.owned_total;
   });

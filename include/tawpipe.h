@@ -38,7 +38,8 @@ extern "C" {
                                  * about to be computed on does not carry the version tag (unit, step)  *
                                  * of that layer, or -- end-of-step check of the NVLink peer path -- a  *
                                  * sequence flag a peer wrote does not end at the value the schedule    *
-                                 * implies (a lost, duplicated or mis-numbered signal)                  */
+                                 * implies (a lost, duplicated or mis-numbered signal), or the step's   *
+                                 * byte ledger differs from the planned schedule's (tawpipe_plan)       */
 #define TAWPIPE_ERUNTIME   -4   /* CUDA or NCCL runtime error (SPEC.md:515 exit code 4)              */
 #define TAWPIPE_EUNINIT    -5   /* call before tawpipe_bootstrap / tawpipe_init                       */
 

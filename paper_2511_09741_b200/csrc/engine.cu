@@ -700,6 +700,15 @@ bool fault_gdone_plus1() {
   }();
   return on;
 }
+// test-only fault (TAWPIPE_FAULT=skip-e-gather): the peer path's E gather leaves the ledger unaccounted, as a schedule
+// that dropped that transfer would -- the end-of-step ledger = plan check must fail the step
+bool fault_skip_e_gather() {
+  static const bool on = [] {
+    const char* e = std::getenv("TAWPIPE_FAULT");
+    return e && std::string(e) == "skip-e-gather";
+  }();
+  return on;
+}
 inline uint32_t* flag_at(int dst_rank, int kind, int src_rank) {
   return static_cast<uint32_t*>(g->peer[dst_rank][PB_SIG]) + kind * kSigRanks + src_rank;
 }
@@ -789,7 +798,7 @@ void gather_p2p(int uid, int slot) {
   }
   if (c.G > 1 && !u.owned && u.cls == U_BLOCK) signal_group(SK_WDONE, seq, s);
   c.nvl_w_bytes += static_cast<double>(u.owned ? c.G - 1 : c.G) * sb;
-  ledger_gather(u, c.G, c.D, c.ledger);
+  if (!(u.cls == U_E && fault_skip_e_gather())) ledger_gather(u, c.G, c.D, c.ledger);
 }
 
 void reduce_p2p(int uid, int slot, float* gacc) {

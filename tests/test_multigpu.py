@@ -152,3 +152,19 @@ def test_peer_flag_invariant_catches_a_misnumbered_signal(tmp_path):
                        env=dict(os.environ, TAWPIPE_FAULT="gdone+1"))
     out = r.stdout + r.stderr
     assert r.returncode != 0 and "peer flag GDONE" in out and "expected" in out, out[-3000:]
+
+
+def test_ledger_invariant_catches_a_skipped_transfer(tmp_path):
+    """Mutation test of the ledger = plan invariant: with TAWPIPE_FAULT=skip-e-gather the peer path leaves its E
+    gather out of the step's byte ledger (as a schedule that dropped the transfer would); the end-of-step check must
+    fail the step with TAWPIPE_EINVARIANT naming the counter."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
+           "--cfg", json.dumps(dict(C0B, n_layers=2)), "--G", "2", "--N", "2", "--steps", "1", "--dtype", "1",
+           "--out", str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, TAWPIPE_FAULT="skip-e-gather"))
+    out = r.stdout + r.stderr
+    assert r.returncode != 0 and "step ledger counter" in out and "the plan's" in out, out[-3000:]

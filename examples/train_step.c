@@ -1,7 +1,9 @@
 /* train_step.c -- the TawPipe step driven from C through include/tawpipe.h alone (no Python in the process).
  *
- * One process = one GPU (world size 1; a multi-rank job would distribute tawpipe_get_unique_id's 128 bytes with its
- * own launcher and call tawpipe_bootstrap(rank, world, device, id) on every rank).
+ * One process per GPU.  World size 1 by default; for a multi-rank job set TAWPIPE_RANK, TAWPIPE_WORLD, TAWPIPE_GROUP
+ * (group size G) and TAWPIPE_ID_FILE in each process's environment: rank 0 writes the 128-byte NCCL unique id
+ * (tawpipe_get_unique_id) to that file, the other ranks wait for it, and every rank calls
+ * tawpipe_bootstrap(rank, world, device = rank, id) -- no torch.distributed involved.
  *
  *   train_step L H n_h I V S B n_micro dtype steps tokens.i32 [weights.f32|-] [shard_out.f32]
  *
@@ -20,6 +22,8 @@
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
 
 #include "tawpipe.h"
 
@@ -36,6 +40,35 @@ static void* read_file(const char* path, long* bytes) {
   }
   fclose(f);
   return p;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+/* rank 0 publishes the NCCL unique id through a file (written under a temporary name, then renamed, so a reader
+ * never sees a partial id); the other ranks poll for it for up to 60 s */
+static int exchange_id(int rank, const char* path, char id[128]) {
+  if (rank == 0) {
+    if (tawpipe_get_unique_id(id) != TAWPIPE_OK) return -1;
+    char tmp[4096];
+    snprintf(tmp, sizeof(tmp), "%s.tmp", path);
+    FILE* f = fopen(tmp, "wb");
+    if (!f || fwrite(id, 1, 128, f) != 128) return -1;
+    fclose(f);
+    return rename(tmp, path);
+  }
+  for (int i = 0; i < 6000; ++i) {
+    FILE* f = fopen(path, "rb");
+    if (f) {
+      const size_t n = fread(id, 1, 128, f);
+      fclose(f);
+      if (n == 128) return 0;
+    }
+    usleep(10000);
+  }
+  return -1;
 }
 
 static int fail(const char* what) {
@@ -77,8 +110,19 @@ int main(int argc, char** argv) {
     return 2;
   }
 
-  if (tawpipe_bootstrap(0, 1, 0, NULL) != TAWPIPE_OK) return fail("tawpipe_bootstrap");
-  if (tawpipe_init(1, 1, L, &d, n_micro) != TAWPIPE_OK) return fail("tawpipe_init");
+  const int rank = env_int("TAWPIPE_RANK", 0), world = env_int("TAWPIPE_WORLD", 1);
+  const int group = env_int("TAWPIPE_GROUP", world);
+  char id[128];
+  memset(id, 0, sizeof(id));
+  if (world > 1) {
+    const char* id_file = getenv("TAWPIPE_ID_FILE");
+    if (!id_file || exchange_id(rank, id_file, id) != 0) {
+      fprintf(stderr, "rank %d: NCCL unique id exchange through TAWPIPE_ID_FILE failed\n", rank);
+      return 2;
+    }
+  }
+  if (tawpipe_bootstrap(rank, world, rank, world > 1 ? id : NULL) != TAWPIPE_OK) return fail("tawpipe_bootstrap");
+  if (tawpipe_init(world, group, L, &d, n_micro) != TAWPIPE_OK) return fail("tawpipe_init");
   if (argc > 12 && argv[12][0] != '-') {
     long w_bytes = 0;
     float* w = (float*)read_file(argv[12], &w_bytes);

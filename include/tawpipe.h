@@ -261,8 +261,8 @@ int tawpipe_rmsnorm_fwd(int dtype, int64_t rows, int H, const void* x, const voi
                         float* rstd, void* stream);
 
 /* RMSNorm backward: dx = (res ? res : 0) + rstd·(dy⊙γ) − x·rstd³·mean_H(dy⊙γ⊙x) written to dx [rows, H];
- * dgamma_acc [H] fp32 += Σ_rows dy⊙x·rstd (accumulated, caller zeroes it).  res nullable (the residual stream
- * gradient added in the same pass). */
+ * dgamma_acc [H] fp32 += Σ_rows dy⊙x·rstd (accumulated, caller zeroes it; row-block partial sums added in block
+ * order, so the result is bit-reproducible).  res nullable (the residual stream gradient added in the same pass). */
 int tawpipe_rmsnorm_bwd(int dtype, int64_t rows, int H, const void* dy, const void* x, const void* gamma,
                         const float* rstd, const void* res, void* dx, float* dgamma_acc, void* stream);
 

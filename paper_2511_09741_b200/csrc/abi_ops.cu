@@ -177,12 +177,16 @@ int tawpipe_rmsnorm_bwd(int dtype, int64_t rows, int H, const void* dy, const vo
                         const float* rstd, const void* res, void* dx, float* dgamma_acc, void* stream) {
   return guarded([&] {
     check_dtype(dtype);
+    cudaStream_t s = as_stream(stream);
+    float* scratch = nullptr;   // dγ row-block partials, stream-ordered allocation for this call
+    TP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), rmsnorm_bwd_scratch_floats(rows, H) * 4, s));
     if (dtype == TAWPIPE_BF16)
       rmsnorm_bwd<bf16>((const bf16*)dy, (const bf16*)x, (const bf16*)gamma, rstd, (const bf16*)res, (bf16*)dx,
-                        dgamma_acc, rows, H, as_stream(stream));
+                        dgamma_acc, scratch, rows, H, s);
     else
       rmsnorm_bwd<float>((const float*)dy, (const float*)x, (const float*)gamma, rstd, (const float*)res, (float*)dx,
-                         dgamma_acc, rows, H, as_stream(stream));
+                         dgamma_acc, scratch, rows, H, s);
+    TP_CUDA(cudaFreeAsync(scratch, s));
   });
 }
 

@@ -107,10 +107,12 @@ void embed_bwd(const int32_t* tok, int64_t tok_stride_seq, int B, int S, const v
                float* dE, void* scratch, size_t scratch_bytes, cudaStream_t s);
 template <typename T>
 void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s);
-// dx = (res ? res : 0) + RMSNorm'(dy); dg_acc += Σ_rows dy⊙x⊙r (fp32)
+// dx = (res ? res : 0) + RMSNorm'(dy); dg_acc += Σ_rows dy⊙x⊙r (fp32).  The row-block partial sums of dγ go to
+// dg_scratch (≥ rmsnorm_bwd_scratch_floats(rows, H) floats) and are added in block order: deterministic
+size_t rmsnorm_bwd_scratch_floats(int64_t rows, int H);
 template <typename T>
 void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
-                 int64_t rows, int H, cudaStream_t s);
+                 float* dg_scratch, int64_t rows, int H, cudaStream_t s);
 template <typename T>
 void rope_apply(T* qkv, int B, int S, int nh, int dh, const float* cos, const float* sin, bool inverse, int ncols_blocks,
                 cudaStream_t s);

@@ -135,7 +135,8 @@ struct Ctx {
   double* d_loss = nullptr;
   double* h_loss = nullptr;
   uint64_t ledger[TAWPIPE_LEDGER_N] = {};
-  uint64_t ledger_plan[TAWPIPE_LEDGER_N] = {};   // what the documented schedule moves per step (plan_ledger)
+  uint64_t ledger_plan[TAWPIPE_LEDGER_N] = {};
+  float* dg_scratch = nullptr;   // RMSNorm dγ row-block partials (rmsnorm_bwd_scratch_floats(T, H))   // what the documented schedule moves per step (plan_ledger)
   int step_t = 0;
   // NVLink peer path of the GWPS schedule (peer.cu): IPC-mapped buffers of every rank, sequence flags
   bool p2p = false;
@@ -342,9 +343,9 @@ void k_rmsnorm_bwd(const void* dy, const void* x, const void* gm, const float* r
                    float* dgacc, int64_t rows, cudaStream_t s) {
   Timed t(s, 4, 0);
   BY_TYPE(rmsnorm_bwd<float>((const float*)dy, (const float*)x, (const float*)gm, r, (const float*)res, (float*)dx,
-                             dgacc, rows, g->H, s),
+                             dgacc, g->dg_scratch, rows, g->H, s),
           rmsnorm_bwd<bf16>((const bf16*)dy, (const bf16*)x, (const bf16*)gm, r, (const bf16*)res, (bf16*)dx, dgacc,
-                            rows, g->H, s));
+                            g->dg_scratch, rows, g->H, s));
 }
 void k_rope(void* qkv, bool inverse, cudaStream_t s) {
   Timed t(s, 4, 0);
@@ -1596,6 +1597,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
   TP_CUDA(cudaMemsetAsync(c.gacc[0], 0, c.units[0].n_pad * 4, c.cs));
   TP_CUDA(cudaMemsetAsync(c.gacc[1], 0, c.units[0].n_pad * 4, c.cs));
   TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.units[L + 1].n_pad * 4, c.cs));   // padding stays zero (nothing writes it)
+  c.dg_scratch = (float*)dmalloc(rmsnorm_bwd_scratch_floats(c.T, c.H) * 4);
   if (G > 1 || D > 1) c.gwire = dmalloc(c.max_pad * esz);
   if (G > 1) c.rsout = dmalloc(c.max_s * esz);
   if (D > 1) c.crecv = dmalloc(c.max_s * (D - 1) * esz);

@@ -87,7 +87,7 @@ template <typename T, int NT, int RB>
 __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                          const T* __restrict__ g, const float* __restrict__ rstd,
                                                          const T* __restrict__ res, T* __restrict__ dx,
-                                                         float* __restrict__ dg_acc, int64_t rows, int H) {
+                                                         float* __restrict__ dg_out, int64_t rows, int H) {
   extern __shared__ float dg_part[];  // [H]
   __shared__ float red[NT / 32];
   for (int c = threadIdx.x; c < H; c += NT) dg_part[c] = 0.f;
@@ -112,7 +112,16 @@ __global__ void __launch_bounds__(NT) rmsnorm_bwd_kernel(const T* __restrict__ d
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < H; c += NT) atomicAdd(&dg_acc[c], dg_part[c]);
+  for (int c = threadIdx.x; c < H; c += NT) dg_out[blockIdx.x * static_cast<int64_t>(H) + c] = dg_part[c];   // block partial
+}
+
+// dg_acc[c] += Σ_b part[b][c], blocks in order (the deterministic second stage of both dγ paths)
+__global__ void dgamma_sum_kernel(const float* __restrict__ part, int nb, int H, float* __restrict__ dg_acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= H) return;
+  float acc = 0.f;
+  for (int b = 0; b < nb; ++b) acc += part[static_cast<int64_t>(b) * H + c];
+  dg_acc[c] += acc;
 }
 
 // ------------------------------------------------------------------------------------ RoPE (rotate-half)
@@ -582,10 +591,11 @@ __global__ void __launch_bounds__(THREADS) rmsnorm_bwd_dx_row_kernel(const bf16*
   }
 }
 
-// dγ_c += Σ_rows dy_rc · x_rc · r_r : block = 8 warps over a 256-column block and a 256-row chunk
+// chunk_part[chunk][c] = Σ_{rows of the chunk} dy_rc · x_rc · r_r : block = 8 warps over a 256-column block and a
+// 256-row chunk (dgamma_sum_kernel adds the chunks in order)
 __global__ void rmsnorm_dgamma_v8_kernel(const bf16* __restrict__ dy, const bf16* __restrict__ x,
-                                         const float* __restrict__ rstd, float* __restrict__ dg_acc, int64_t rows,
-                                         int H) {
+                                         const float* __restrict__ rstd, float* __restrict__ chunk_part,
+                                         int64_t rows, int H) {
   __shared__ float part[8][256];
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int c0 = blockIdx.x * 256 + lane * 8;
@@ -604,7 +614,7 @@ __global__ void rmsnorm_dgamma_v8_kernel(const bf16* __restrict__ dy, const bf16
   __syncthreads();
   const float v = part[0][threadIdx.x] + part[1][threadIdx.x] + part[2][threadIdx.x] + part[3][threadIdx.x] +
                   part[4][threadIdx.x] + part[5][threadIdx.x] + part[6][threadIdx.x] + part[7][threadIdx.x];
-  atomicAdd(&dg_acc[blockIdx.x * 256 + threadIdx.x], v);
+  chunk_part[blockIdx.y * static_cast<int64_t>(H) + blockIdx.x * 256 + threadIdx.x] = v;
 }
 
 // Single-pass cross-entropy for bf16 logits, V % 8 == 0 and V ≤ 8·NT·NV: the row is read once into registers (16-byte
@@ -711,9 +721,14 @@ void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H,
   rmsnorm_fwd_kernel<T, 256><<<static_cast<unsigned>(rows), 256, 0, s>>>(x, g, y, rstd, H, eps);
   LAUNCHED();
 }
+size_t rmsnorm_bwd_scratch_floats(int64_t rows, int H) {   // the generic path's 32-row blocks bound both paths
+  return static_cast<size_t>(blocks_for(rows, 32)) * static_cast<size_t>(H);
+}
+
 template <typename T>
 void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
-                 int64_t rows, int H, cudaStream_t s) {
+                 float* dg_scratch, int64_t rows, int H, cudaStream_t s) {
+  TP_CHECK(dg_scratch != nullptr, TAWPIPE_ECONFIG, "rmsnorm_bwd: dγ scratch is NULL");
   if constexpr (std::is_same<T, bf16>::value) {
     if (H % 256 == 0 && (H == 256 || H == 1024 || H == 2048 || H == 4096 || H == 5120)) {
       const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
@@ -731,8 +746,11 @@ void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T
           break;
       }
       LAUNCHED();
-      rmsnorm_dgamma_v8_kernel<<<dim3(H / 256, static_cast<unsigned>((rows + 255) / 256)), 256, 0, s>>>(
-          dy, x, rstd, dg_acc, rows, H);
+      const int nb = static_cast<int>((rows + 255) / 256);
+      rmsnorm_dgamma_v8_kernel<<<dim3(H / 256, static_cast<unsigned>(nb)), 256, 0, s>>>(dy, x, rstd, dg_scratch,
+                                                                                        rows, H);
+      LAUNCHED();
+      dgamma_sum_kernel<<<(H + 255) / 256, 256, 0, s>>>(dg_scratch, nb, H, dg_acc);
       LAUNCHED();
       return;
     }
@@ -743,7 +761,10 @@ void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T
     TP_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel<T, 256, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   }
-  rmsnorm_bwd_kernel<T, 256, RB><<<blocks_for(rows, RB), 256, smem, s>>>(dy, x, g, rstd, res, dx, dg_acc, rows, H);
+  const unsigned nb = blocks_for(rows, RB);
+  rmsnorm_bwd_kernel<T, 256, RB><<<nb, 256, smem, s>>>(dy, x, g, rstd, res, dx, dg_scratch, rows, H);
+  LAUNCHED();
+  dgamma_sum_kernel<<<(H + 255) / 256, 256, 0, s>>>(dg_scratch, static_cast<int>(nb), H, dg_acc);
   LAUNCHED();
 }
 template <typename T>
@@ -859,7 +880,7 @@ void adamw_grouped(const GradSources& src, float* master, float* m, float* v, W*
 #define INST(T)                                                                                                    \
   template void embed_fwd<T>(const int32_t*, int64_t, int, int, const T*, int, T*, cudaStream_t);                \
   template void rmsnorm_fwd<T>(const T*, const T*, T*, float*, int64_t, int, float, cudaStream_t);              \
-  template void rmsnorm_bwd<T>(const T*, const T*, const T*, const float*, const T*, T*, float*, int64_t, int,   \
+  template void rmsnorm_bwd<T>(const T*, const T*, const T*, const float*, const T*, T*, float*, float*, int64_t, int,   \
                                cudaStream_t);                                                                    \
   template void rope_apply<T>(T*, int, int, int, int, const float*, const float*, bool, int, cudaStream_t);     \
   template void swiglu_fwd<T>(const T*, T*, int64_t, int, cudaStream_t);                                         \

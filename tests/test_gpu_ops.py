@@ -82,6 +82,26 @@ def test_rmsnorm_fwd_bwd_matches_oracle(T, dtype, rows, H):
         assert rel(host(dg) - 0.5, rdg) < (1e-5 if dtype == F32 else 1e-4)
 
 
+@pytest.mark.parametrize("dtype,rows,H", [(BF, 32768, 4096), (F32, 1000, 96)])   # v8 chunk path / generic path
+def test_rmsnorm_bwd_dgamma_is_bit_reproducible(T, dtype, rows, H):
+    """dγ's row-block partial sums are added in block order (no atomics): two runs give identical bits."""
+    rng = np.random.default_rng(rows + H)
+    x, _ = dev(rng.standard_normal((rows, H)), dtype)
+    g, _ = dev(1.0 + 0.1 * rng.uniform(-1, 1, H), dtype)
+    dy, _ = dev(rng.standard_normal((rows, H)), dtype)
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, dtype=torch.float32, device="cuda")
+    T.rmsnorm_fwd(dtype, rows, H, x.data_ptr(), g.data_ptr(), 1e-5, y.data_ptr(), rstd.data_ptr())
+    outs = []
+    for _ in range(2):
+        dx = torch.empty_like(x)
+        dg = torch.zeros(H, dtype=torch.float32, device="cuda")
+        T.rmsnorm_bwd(dtype, rows, H, dy.data_ptr(), x.data_ptr(), g.data_ptr(), rstd.data_ptr(), None,
+                      dx.data_ptr(), dg.data_ptr())
+        outs.append(host(dg))
+    assert np.array_equal(outs[0], outs[1])
+
+
 # ---------------------------------------------------------------------------------------------- RoPE
 @pytest.mark.parametrize("dtype,B,S,nh,dh", [(F32, 2, 200, 3, 64), (F32, 1, 128, 2, 16), (BF, 1, 384, 4, 128),
                                              (BF, 2, 256, 32, 128), (BF, 1, 256, 4, 64), (BF, 1, 64, 2, 32)])

@@ -154,6 +154,28 @@ def test_bf16_multichunk_head_step_matches_oracle(T):
     run_parity(T, base, T.BF16, 1e-2, 2e-2, 5e-2, n_micro=1, steps=2, hyper=LINEAR)
 
 
+def test_c0_fp32_step_is_bit_reproducible(T):
+    """The fp32 path has no order-dependent reduction left (SIMT GEMMs and attention, sorted embedding backward,
+    in-order dγ partials, fused AdamW): two fresh sessions on the same inputs give bit-identical losses and weights.
+    (The bf16 path's attention backward adds dQ partials by TMA reduce-add in arrival order, R25.)"""
+    cfg = oracle_cfg(C0)
+    params = synth.perturb_gains(synth.init_params(cfg.n_layers, cfg.hidden, cfg.ffn, cfg.vocab))
+    runs = []
+    for _ in range(2):
+        dims = T.ModelDims(n_layers=cfg.n_layers, hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, vocab=cfg.vocab,
+                           seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=T.FP32)
+        sess = T.Session(1, 1, dims, 4)
+        try:
+            sess.load(T.pack_full_model(params))
+            losses = [sess.step(synth.tokens(4, cfg.micro_bs, cfg.seq, cfg.vocab, step=s)) for s in range(2)]
+            runs.append((losses, sess.shard()))
+        finally:
+            sess.close()
+            T.bootstrap(0, 1, 0)
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
+
+
 def test_trace_export_and_idle_fraction(T):
     """NEXT-4: the Trace-Event JSON of a timed step is well formed and consistent with the step's own timing."""
     cfg = oracle_cfg(C0B)

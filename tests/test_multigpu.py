@@ -67,6 +67,18 @@ def free_port():
         return s.getsockname()[1]
 
 
+def run_torchrun(cmd, env, timeout=300):
+    """Run a torchrun command; the probed free port can be taken between probing and torchrun's bind, so retry with a
+    new port on EADDRINUSE."""
+    for _ in range(3):
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+        if "EADDRINUSE" not in r.stderr:
+            return r
+        i = next(k for k, c in enumerate(cmd) if c.startswith("--master-port="))
+        cmd[i] = f"--master-port={free_port()}"
+    return r
+
+
 @pytest.mark.parametrize("name,base,P,G,L,N,dtype,ckpt,no_cco,ring,emu_gbps,emu_node,linear", CASES,
                          ids=[c[0] for c in CASES])
 def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, ckpt, no_cco, ring, emu_gbps, emu_node,
@@ -85,11 +97,7 @@ def test_multigpu_step_matches_oracle(tmp_path, name, base, P, G, L, N, dtype, c
         + (["--ring"] if ring else []) + (["--literal"] if literal else []) + (["--linear"] if linear else []) \
         + (["--emu-gbps", str(emu_gbps), "--emu-node", str(emu_node)] if emu_gbps else [])
     env = dict(os.environ, TAWPIPE_COMM="nccl") if name.endswith("-nccl") else dict(os.environ)
-    for _ in range(3):   # the free port can be taken between probing and torchrun's bind: retry on EADDRINUSE
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
-        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
-            break
-        cmd[cmd.index(next(c for c in cmd if c.startswith("--master-port=")))] = f"--master-port={free_port()}"
+    r = run_torchrun(cmd, env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = [np.load(tmp_path / f"rank{i}.npz") for i in range(P)]
     # which implementation ran: the peer path for GWPS unless forced to NCCL; ring / literal always NCCL
@@ -148,8 +156,7 @@ def test_peer_flag_invariant_catches_a_misnumbered_signal(tmp_path):
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--cfg", json.dumps(dict(C0B, n_layers=2)), "--G", "2", "--N", "2", "--steps", "1", "--dtype", "1",
            "--out", str(tmp_path)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
-                       env=dict(os.environ, TAWPIPE_FAULT="gdone+1"))
+    r = run_torchrun(cmd, dict(os.environ, TAWPIPE_FAULT="gdone+1"))
     out = r.stdout + r.stderr
     assert r.returncode != 0 and "peer flag GDONE" in out and "expected" in out, out[-3000:]
 
@@ -164,7 +171,6 @@ def test_ledger_invariant_catches_a_skipped_transfer(tmp_path):
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--cfg", json.dumps(dict(C0B, n_layers=2)), "--G", "2", "--N", "2", "--steps", "1", "--dtype", "1",
            "--out", str(tmp_path)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300,
-                       env=dict(os.environ, TAWPIPE_FAULT="skip-e-gather"))
+    r = run_torchrun(cmd, dict(os.environ, TAWPIPE_FAULT="skip-e-gather"))
     out = r.stdout + r.stderr
     assert r.returncode != 0 and "step ledger counter" in out and "the plan's" in out, out[-3000:]

@@ -419,7 +419,7 @@ def run_ours(args, c):
         # w/o GWPS = the group scheduler replaced by WeiPipe's ring exchange, i.e. weipipe_ring above
         out["ablations"] = {"wo_gwps": "baselines.weipipe_ring", "wo_cco": "baselines.tawpipe_wo_cco"}
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only (bench contract)
             try:
                 out["cpu_baseline"] = oracle_baseline(c, budget_s=20.0)
             except Exception as e:

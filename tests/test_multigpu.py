@@ -55,7 +55,16 @@ CASES += [("c0-2x2-nccl", C0, 4, 2, 2, 4, 0, 0, False, False, 0.0, 0),
           ("c0b-4x1-L8-bf16", C0B, 4, 1, 8, 4, 1, 1, False, False, 0.0, 0),
           ("c0b-4x1-L8-bf16-nccl", C0B, 4, 1, 8, 4, 1, 1, False, False, 0.0, 0),
           ("c0b-2x2-L4-bf16-nccl", C0B, 4, 2, 4, 8, 1, 2, False, False, 0.0, 0),
-          ("c0-4x1-L8-fp32", C0, 4, 1, 8, 4, 0, 1, False, False, 0.0, 0)]
+          ("c0-4x1-L8-fp32", C0, 4, 1, 8, 4, 0, 1, False, False, 0.0, 0),
+          # P = 8 (skipped below 8 GPUs): the headline 4 x 2 split, D = 8 groups of 1, 2 x 4, the FSDP-style 1 x 8,
+          # the ring and the paper-literal mode at P = 8
+          ("c0-4x2-p8", C0, 8, 2, 4, 8, 0, 0, False, False, 0.0, 0),
+          ("c0b-4x2-p8-bf16", C0B, 8, 2, 8, 8, 1, 1, False, False, 0.0, 0),
+          ("c0-8x1-p8", C0, 8, 1, 8, 8, 0, 0, False, False, 0.0, 0),
+          ("c0-2x4-p8", C0, 8, 4, 2, 8, 0, 0, False, False, 0.0, 0),
+          ("c0-1x8-fsdp-p8", C0, 8, 8, 2, 8, 0, 0, False, False, 0.0, 0),
+          ("c0-ring8", C0, 8, 1, 8, 8, 0, 0, False, True, 0.0, 0),
+          ("c0-literal-4x2-p8", C0, 8, 2, 8, 8, 0, 0, False, "literal", 0.0, 0)]
 CASES = [c + (True,) for c in CASES] + [("c0-2x2-default-eps", C0, 4, 2, 2, 4, 0, 0, False, False, 0.0, 0, False),
                                        ("c0b-1x2-bf16-default-eps", C0B, 2, 2, 2, 2, 1, 0, False, False, 0.0, 0,
                                         False)]

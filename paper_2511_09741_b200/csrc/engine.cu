@@ -135,8 +135,8 @@ struct Ctx {
   double* d_loss = nullptr;
   double* h_loss = nullptr;
   uint64_t ledger[TAWPIPE_LEDGER_N] = {};
-  uint64_t ledger_plan[TAWPIPE_LEDGER_N] = {};
-  float* dg_scratch = nullptr;   // RMSNorm dγ row-block partials (rmsnorm_bwd_scratch_floats(T, H))   // what the documented schedule moves per step (plan_ledger)
+  uint64_t ledger_plan[TAWPIPE_LEDGER_N] = {};   // what the documented schedule moves per step (plan_ledger)
+  float* dg_scratch = nullptr;   // RMSNorm dγ row-block partials (rmsnorm_bwd_scratch_floats(T, H))
   int step_t = 0;
   // NVLink peer path of the GWPS schedule (peer.cu): IPC-mapped buffers of every rank, sequence flags
   bool p2p = false;
@@ -1003,8 +1003,8 @@ void layer_forward(int l, int mb, void* W, bool write_out) {
 }
 
 // Gradient accumulators are not zeroed by a full memset per layer: the first micro-batch's wgrad GEMMs store
-// (EPI_F32_STORE) and the later ones accumulate; only the two RMSNorm-gain ranges (atomic partial sums) are zeroed
-// (gacc_store_first).  0 + x == x in fp32, so the values are identical to memset + accumulate.
+// (EPI_F32_STORE) and the later ones accumulate; only the two RMSNorm-gain ranges (which the norm backward adds
+// into) are zeroed (gacc_store_first).  0 + x == x in fp32, so the values are identical to memset + accumulate.
 bool gacc_store_first() {
   static const bool on = [] {
     const char* e = std::getenv("TAWPIPE_GACC_ZERO");
@@ -1248,7 +1248,7 @@ double run_step(const int32_t* tokens, bool device_tokens) {
   // ---- head F (a6)
   wait_on(c.cs, c.evF);
   if (gacc_store_first())
-    TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.H * 4, c.cs));   // final-norm gain (atomic partial sums)
+    TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.H * 4, c.cs));   // final-norm gain (the norm backward adds into it)
   else
     TP_CUDA(cudaMemsetAsync(c.gaccF, 0, c.units[F].n_pad * 4, c.cs));
   void* Fbuf = unit_buffer(F, 0);

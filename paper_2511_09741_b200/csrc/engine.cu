@@ -84,7 +84,7 @@ struct TimedRegion {
   cudaEvent_t a, b;
   int kind;  // 0 gemm, 1 attention, 2 adamw, 3 exposed wait, 4 elementwise, 5 weight comm, 6 grad comm
   double work;
-  int stream;  // 0 compute, 1 weights, 2 gradients, 3 weight-gradient GEMMs (compute work on the wgrad stream)
+  int stream;  // 0 compute, 1 weights, 2 gradients
 };
 
 struct Ctx {
@@ -102,7 +102,6 @@ struct Ctx {
   size_t esz = 4;
   ncclComm_t wg = nullptr, wr = nullptr, gg = nullptr, gr = nullptr;
   cudaStream_t cs = nullptr, ws = nullptr, gs = nullptr;
-  cudaStream_t wgs = nullptr;   // weight-gradient GEMMs of the layer backward, beside the dgrad chain on cs
   std::vector<Unit> units;  // 0..L-1 layers, L = E, L+1 = F
   int64_t owned_total = 0, max_pad = 0, max_s = 0;
   float *master = nullptr, *mom = nullptr, *vel = nullptr;
@@ -154,7 +153,6 @@ struct Ctx {
   // events
   cudaEvent_t w_ready[2], w_free[2], g_ready[2], g_free[2], evE, evF, evGF, evGE, ev_s0, ev_s1, ev_ws0, ev_ws1,
       ev_gs0, ev_gs1;
-  cudaEvent_t ev_wg_in[4], ev_wg_dh, ev_wg_done;   // wgrad stream: inputs ready, dh read, all done
   // timing
   bool timing = false;
   std::vector<TimedRegion> regions;
@@ -231,7 +229,7 @@ struct Timed {  // RAII CUDA-event bracket on a stream (only when timing is enab
     r.b = pool_event();
     r.kind = kind;
     r.work = work;
-    r.stream = st == g->cs ? 0 : st == g->ws ? 1 : st == g->wgs ? 3 : 2;
+    r.stream = st == g->cs ? 0 : st == g->ws ? 1 : 2;
     TP_CUDA(cudaEventRecord(r.a, s));
   }
   // never throws: a destructor that runs while an exception unwinds must not raise a second one (that would
@@ -1015,29 +1013,9 @@ bool gacc_store_first() {
   return on;
 }
 
-// The four weight-gradient GEMMs run on their own stream (wgs) beside the dgrad chain on cs: each waits for its
-// inputs on cs, so the persistent GEMMs' last partial waves (3.5 waves for the O wgrad at C3) overlap the next
-// dgrad / attention kernels instead of leaving SMs idle.  cs waits for the down-projection wgrad before it
-// overwrites dh, and for all four at the end of the layer (the scratch activations and gradients they read are
-// reused by the next one).  TAWPIPE_WGRAD_STREAM=0 runs them in line on cs.
-bool wgrad_stream() {
-  static const bool on = [] {
-    const char* e = std::getenv("TAWPIPE_WGRAD_STREAM");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 void layer_backward(int l, int mb, void* W, float* G_, bool first) {
   cudaStream_t s = g->cs;
   const bool acc = !(first && gacc_store_first());
-  const bool side = wgrad_stream();
-  cudaStream_t ws2 = side ? g->wgs : s;
-  auto fork = [&](int i) {   // the wgrad stream waits for the inputs cs has produced so far
-    if (!side) return;
-    TP_CUDA(cudaEventRecord(g->ev_wg_in[i], s));
-    TP_CUDA(cudaStreamWaitEvent(ws2, g->ev_wg_in[i], 0));
-  };
   const int64_t T = g->T, H = g->H, I = g->I;
   LayerW w = layer_weights(W);
   // recompute from the checkpoint h_l; the last layer's last micro-batch is still resident in the
@@ -1052,9 +1030,7 @@ void layer_backward(int l, int mb, void* W, float* G_, bool first) {
   float* ggu = G_ + 2 * H + 4 * H * H;     // Wgate|Wup [2I, H]
   float* gd = G_ + 2 * H + 4 * H * H + 2 * I * H;  // Wdown [H, I]
   // h2 = h1 + y·Wdownᵀ
-  fork(0);
-  gemm(H, I, T, dh, H, false, A.y, I, false, gd, I, true, acc, nullptr, ws2);
-  if (side) TP_CUDA(cudaEventRecord(g->ev_wg_dh, ws2));
+  gemm(H, I, T, dh, H, false, A.y, I, false, gd, I, true, acc, nullptr, s);
   if (g->bf && !gemm_force_simt()) {
     // dgrad of the down projection with the SwiGLU backward in the epilogue: dY never reaches HBM
     GemmArgs a{T, I, H, dh, H, true, w.wdown, I, false, g->dGU, 2 * I, false, false, nullptr};
@@ -1070,25 +1046,17 @@ void layer_backward(int l, int mb, void* W, float* G_, bool first) {
     BY_TYPE(swiglu_bwd<float>((const float*)g->dY, (const float*)A.gu, (float*)g->dGU, T, (int)I, s),
             swiglu_bwd<bf16>((const bf16*)g->dY, (const bf16*)A.gu, (bf16*)g->dGU, T, (int)I, s));
   }
-  fork(1);
-  gemm(2 * I, H, T, g->dGU, 2 * I, false, A.b, H, false, ggu, H, true, acc, nullptr, ws2);
+  gemm(2 * I, H, T, g->dGU, 2 * I, false, A.b, H, false, ggu, H, true, acc, nullptr, s);
   gemm(T, H, 2 * I, g->dGU, 2 * I, true, w.wgu, H, false, g->db, H, false, false, nullptr, s);
   k_rmsnorm_bwd(g->db, A.h1, w.mlp_norm, A.r2, dh, g->dh1, gmn, T, s);
   // h1 = h + o·Woᵀ
-  fork(2);
-  gemm(H, H, T, g->dh1, H, false, A.o, H, false, go, H, true, acc, nullptr, ws2);
+  gemm(H, H, T, g->dh1, H, false, A.o, H, false, go, H, true, acc, nullptr, s);
   gemm(T, H, H, g->dh1, H, true, w.wo, H, false, g->dO, H, false, false, nullptr, s);
   attn_bwd(A.qkv, A.o, A.lse, g->dO, g->dqkv, s);
   if (!use_tc_attention()) k_rope(g->dqkv, true, s);   // the tcgen05 backward applies it in its epilogues
-  fork(3);
-  gemm(3 * H, H, T, g->dqkv, 3 * H, false, A.a, H, false, gq, H, true, acc, nullptr, ws2);
+  gemm(3 * H, H, T, g->dqkv, 3 * H, false, A.a, H, false, gq, H, true, acc, nullptr, s);
   gemm(T, H, 3 * H, g->dqkv, 3 * H, true, w.wqkv, H, false, g->da, H, false, false, nullptr, s);
-  if (side) TP_CUDA(cudaStreamWaitEvent(s, g->ev_wg_dh, 0));   // the down-projection wgrad has read dh
   k_rmsnorm_bwd(g->da, hin, w.attn_norm, A.r1, g->dh1, dh, G_, T, s);
-  if (side) {   // join: the next micro-batch / layer reuses every buffer the wgrads read
-    TP_CUDA(cudaEventRecord(g->ev_wg_done, ws2));
-    TP_CUDA(cudaStreamWaitEvent(s, g->ev_wg_done, 0));
-  }
 }
 
 // a6: final RMSNorm + LM head + cross-entropy, forward and backward back to back, in row chunks
@@ -1131,10 +1099,9 @@ __global__ void split_tokens_kernel(const int32_t* __restrict__ tok, int64_t seq
 
 // ------------------------------------------------------------------------------------ trace export (NEXT-4)
 // Trace-Event JSON ("X" complete events, microseconds from the step's first compute-stream event) of the last
-// timed step: one thread per stream (0 compute, 1 weights, 2 gradients, 3 the weight-gradient GEMMs), pid = rank.
-// otherData carries the step time and, per stream, the busy time (union of its regions; the compute entry is the
-// union of the compute and wgrad streams) and the compute idle ("bubble") fraction: time neither compute stream runs
-// a timed kernel nor the compute stream waits on communication.
+// timed step: one thread per stream (0 compute, 1 weights, 2 gradients), pid = rank.  otherData carries the
+// step time and, per stream, the busy time (union of its regions) and the compute stream's idle ("bubble")
+// fraction: time the compute stream is neither running a timed kernel nor waiting on communication.
 void build_trace_json(float step_ms) {
   Ctx& c = *g;
   static const char* kind_name[7] = {"gemm", "attention", "adamw", "exposed_comm_wait", "elementwise",
@@ -1149,7 +1116,7 @@ void build_trace_json(float step_ms) {
     float t0 = 0.f, t1 = 0.f;
     TP_CUDA(cudaEventElapsedTime(&t0, c.ev_s0, r.a));
     TP_CUDA(cudaEventElapsedTime(&t1, c.ev_s0, r.b));
-    if (r.kind != 3) iv[r.stream == 3 ? 0 : r.stream].push_back({static_cast<double>(t0), static_cast<double>(t1)});
+    if (r.kind != 3) iv[r.stream].push_back({static_cast<double>(t0), static_cast<double>(t1)});
     std::snprintf(buf, sizeof(buf),
                   "%s{\"name\":\"%s\",\"cat\":\"tawpipe\",\"ph\":\"X\",\"ts\":%.3f,\"dur\":%.3f,\"pid\":%d,"
                   "\"tid\":%d,\"args\":{\"work\":%.6g}}",
@@ -1599,10 +1566,7 @@ void build(int P, int G, int L, const tawpipe_dims* d, int N) {
     TP_CUDA(cudaEventCreateWithFlags(&c.g_ready[i], cudaEventDisableTiming));
     TP_CUDA(cudaEventCreateWithFlags(&c.g_free[i], cudaEventDisableTiming));
   }
-  for (cudaEvent_t* e : {&c.evE, &c.evF, &c.evGF, &c.evGE, &c.ev_wg_in[0], &c.ev_wg_in[1], &c.ev_wg_in[2],
-                         &c.ev_wg_in[3], &c.ev_wg_dh, &c.ev_wg_done})
-    TP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  TP_CUDA(cudaStreamCreateWithFlags(&c.wgs, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&c.evE, &c.evF, &c.evGF, &c.evGE}) TP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (cudaEvent_t* e : {&c.ev_s0, &c.ev_s1, &c.ev_ws0, &c.ev_ws1, &c.ev_gs0, &c.ev_gs1}) TP_CUDA(cudaEventCreate(e));
   if (c.world > 1) {
     // group communicator: color k, rank j ; rail communicator: color j, rank k (R5)
@@ -1794,7 +1758,6 @@ void destroy() {
   if (g->cs) cudaStreamDestroy(g->cs);
   if (g->ws) cudaStreamDestroy(g->ws);
   if (g->gs) cudaStreamDestroy(g->gs);
-  if (g->wgs) cudaStreamDestroy(g->wgs);
   delete g;
   g = nullptr;
 }

@@ -190,7 +190,7 @@ def test_trace_export_and_idle_fraction(T):
         st, tr = sess.stats(), sess.trace()
         ev, od = tr["traceEvents"], tr["otherData"]
         names = {"gemm", "attention", "adamw", "exposed_comm_wait", "elementwise", "weight_comm", "grad_comm"}
-        assert ev and all(e["ph"] == "X" and e["name"] in names and e["tid"] in (0, 1, 2, 3) for e in ev)
+        assert ev and all(e["ph"] == "X" and e["name"] in names and e["tid"] in (0, 1, 2) for e in ev)
         step_us = st["step_ms"] * 1e3
         assert all(-1.0 <= e["ts"] and e["ts"] + e["dur"] <= step_us + 1.0 for e in ev)
         assert abs(od["step_ms"] - st["step_ms"]) < 1e-3

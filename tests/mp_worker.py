@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--emu-gbps", type=float, default=0.0)   # NEXT-3 emulated inter-node link
     ap.add_argument("--emu-node", type=int, default=0)
     ap.add_argument("--linear", action="store_true", help="AdamW ε = 1, lr = 1, no decay: update linear in g (R18)")
+    ap.add_argument("--init-only", action="store_true", help="no tawpipe_load, no step: save the device-side init")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     hyper = dict(lr=1.0, adam_eps=1.0, weight_decay=0.0) if a.linear else {}
@@ -41,6 +42,10 @@ def main():
                        schedule=(T.NO_CCO if a.no_cco else T.GWPS) | (T.RING if a.ring else 0)
                        | (T.LITERAL if a.literal else 0), **hyper)
     sess = T.Session(world, a.G, dims, a.N)
+    if a.init_only:   # R20: the seeded device-side initialisation, keyed by canonical position
+        np.savez(os.path.join(a.out, f"rank{rank}.npz"), shard=sess.shard())
+        sess.close()
+        return
     sess.load(T.pack_full_model(params))
     if a.emu_gbps > 0:
         sess.set_link_emulation(a.emu_gbps, 30.0, a.emu_node)

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import synth
-from helpers import C0, C0B, TOL_DELTA, om, oracle_cfg, reassemble, weight_errors
+from helpers import C0, C0B, TOL_DELTA, om, oracle_cfg, reassemble, tensors, weight_errors
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -174,6 +174,33 @@ def test_c0_fp32_step_is_bit_reproducible(T):
             T.bootstrap(0, 1, 0)
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_device_init_statistics_and_reproducibility(T):
+    """R20: without tawpipe_load the library initialises on the device from dims.seed -- matrices, E and the head
+    N(0, 0.02), the RMSNorm gains exactly 1; the same seed gives the same bits, another seed other values."""
+    cfg = oracle_cfg(C0B)
+
+    def init(seed):
+        dims = T.ModelDims(n_layers=cfg.n_layers, hidden=cfg.hidden, heads=cfg.heads, ffn=cfg.ffn, vocab=cfg.vocab,
+                           seq=cfg.seq, micro_bs=cfg.micro_bs, dtype=T.BF16, seed=seed)
+        sess = T.Session(1, 1, dims, 1)
+        try:
+            return reassemble(cfg, 1, 1, [sess.shard()])
+        finally:
+            sess.close()
+            T.bootstrap(0, 1, 0)
+
+    a, b, c = init(7), init(7), init(8)
+    for (name, x), (_, y), (_, z) in zip(tensors(a), tensors(b), tensors(c)):
+        assert np.array_equal(x, y), name
+        if name.endswith("norm"):
+            assert np.all(x == 1.0), name
+            continue
+        assert not np.array_equal(x, z), name
+        n = x.size
+        assert abs(x.mean()) < 5 * 0.02 / np.sqrt(n), (name, x.mean())
+        assert abs(x.std() / 0.02 - 1) < 5 / np.sqrt(2 * n) + 1e-3, (name, x.std())
 
 
 def test_trace_export_and_idle_fraction(T):

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 import synth
-from helpers import C0, C0B, ROOT, TOL_DELTA, om, oracle_cfg, reassemble, weight_errors
+from helpers import C0, C0B, ROOT, TOL_DELTA, om, oracle_cfg, reassemble, tensors, weight_errors
 from oracle import layout as OL
 from oracle import ledger as LG
 
@@ -183,3 +183,24 @@ def test_ledger_invariant_catches_a_skipped_transfer(tmp_path):
     r = run_torchrun(cmd, dict(os.environ, TAWPIPE_FAULT="skip-e-gather"))
     out = r.stdout + r.stderr
     assert r.returncode != 0 and "step ledger counter" in out and "the plan's" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("P,G", [(2, 2), (2, 1)])
+def test_device_init_is_partition_independent(tmp_path, P, G):
+    """R20: the seeded device-side initialisation is a function of the canonical parameter position only, so the
+    stripes P ranks initialise reassemble bit for bit into the model one rank initialises."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    cfg = oracle_cfg(C0B)
+    shards = {}
+    for p, g in ((1, 1), (P, G)):
+        out = tmp_path / f"p{p}g{g}"
+        out.mkdir()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
+               "--cfg", json.dumps(C0B), "--G", str(g), "--N", str(p), "--dtype", "1", "--init-only", "--out", str(out)]
+        r = run_torchrun(cmd, dict(os.environ))
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        shards[p] = reassemble(cfg, p, g, [np.load(out / f"rank{i}.npz")["shard"] for i in range(p)])
+    for (name, a), (_, b) in zip(tensors(shards[1]), tensors(shards[P])):
+        assert np.array_equal(a, b), name

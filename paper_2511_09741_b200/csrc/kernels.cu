@@ -693,11 +693,13 @@ inline unsigned grid_stride_blocks(int64_t n) {
 
 template <typename T>
 void embed_fwd(const int32_t* tok, int64_t stride_seq, int B, int S, const T* E, int H, T* h, cudaStream_t s) {
+  if (static_cast<int64_t>(B) * S <= 0) return;   // empty input: nothing to launch
   embed_fwd_kernel<T><<<static_cast<unsigned>(B) * S, 256, 0, s>>>(tok, stride_seq, S, E, H, h);
   LAUNCHED();
 }
 template <typename T>
 void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
+  if (rows <= 0) return;
   if constexpr (std::is_same<T, bf16>::value) {
     const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
     switch (H) {
@@ -729,6 +731,7 @@ template <typename T>
 void rmsnorm_bwd(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, float* dg_acc,
                  float* dg_scratch, int64_t rows, int H, cudaStream_t s) {
   TP_CHECK(dg_scratch != nullptr, TAWPIPE_ECONFIG, "rmsnorm_bwd: dγ scratch is NULL");
+  if (rows <= 0) return;   // no rows: dx is empty and dγ gains nothing
   if constexpr (std::is_same<T, bf16>::value) {
     if (H % 256 == 0 && (H == 256 || H == 1024 || H == 2048 || H == 4096 || H == 5120)) {
       const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
@@ -812,6 +815,7 @@ void swiglu_bwd(const T* dy, const T* gu, T* dgu, int64_t rows, int I, cudaStrea
 template <typename T>
 void cross_entropy(T* logits, const int32_t* targets, int64_t rows, int V, float inv_denom, float* loss_rows,
                    cudaStream_t s) {
+  if (rows <= 0) return;
   if constexpr (std::is_same<T, bf16>::value) {
     if (V % 8 == 0 && V <= 8 * 512 * 8) {   // up to V = 32,768 in registers
       ce_v8_kernel<512, 8><<<static_cast<unsigned>(rows), 512, 0, s>>>(logits, targets, V, inv_denom, loss_rows);

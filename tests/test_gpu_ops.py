@@ -82,6 +82,30 @@ def test_rmsnorm_fwd_bwd_matches_oracle(T, dtype, rows, H):
         assert rel(host(dg) - 0.5, rdg) < (1e-5 if dtype == F32 else 1e-4)
 
 
+@pytest.mark.parametrize("dtype", [F32, BF])
+def test_empty_inputs_are_no_ops(T, dtype):
+    """Edge case: zero rows / tokens launch nothing and leave every output untouched (no invalid empty grid)."""
+    H, V = 256, 512
+    tdt = torch.float32 if dtype == F32 else torch.bfloat16
+    x = torch.ones(4, H, dtype=tdt, device="cuda")
+    g = torch.ones(H, dtype=tdt, device="cuda")
+    y = torch.full((4, H), 3.0, dtype=tdt, device="cuda")
+    rstd = torch.full((4,), 5.0, device="cuda")
+    T.rmsnorm_fwd(dtype, 0, H, x.data_ptr(), g.data_ptr(), 1e-5, y.data_ptr(), rstd.data_ptr())
+    dg = torch.full((H,), 0.5, device="cuda")
+    T.rmsnorm_bwd(dtype, 0, H, x.data_ptr(), x.data_ptr(), g.data_ptr(), rstd.data_ptr(), None, y.data_ptr(),
+                  dg.data_ptr())
+    z = torch.full((4, V), 2.0, dtype=tdt, device="cuda")
+    tg = torch.zeros(4, dtype=torch.int32, device="cuda")
+    lr = torch.full((4,), 7.0, device="cuda")
+    T.cross_entropy(dtype, 0, V, z.data_ptr(), tg.data_ptr(), 1.0, lr.data_ptr())
+    E = torch.ones(V, H, dtype=tdt, device="cuda")
+    T.embed_fwd(dtype, 1, 0, tg.data_ptr(), 1, E.data_ptr(), H, y.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.all(y == 3.0) and torch.all(rstd == 5.0) and torch.all(dg == 0.5)
+    assert torch.all(z == 2.0) and torch.all(lr == 7.0)
+
+
 @pytest.mark.parametrize("dtype,rows,H", [(BF, 32768, 4096), (F32, 1000, 96)])   # v8 chunk path / generic path
 def test_rmsnorm_bwd_dgamma_is_bit_reproducible(T, dtype, rows, H):
     """dγ's row-block partial sums are added in block order (no atomics): two runs give identical bits."""

@@ -202,7 +202,8 @@ void tawpipe_finalize(void);
  * No context is needed.  Layouts are row-major; "dtype" is TAWPIPE_FP32 (fp32 tensors, SIMT kernels -- the fp32
  * parity path) or TAWPIPE_BF16 (bf16 tensors, fp32 arithmetic inside, tcgen05 where the op is a contraction).
  * Statistics (rstd, LSE, δ, loss rows) and accumulators are always fp32.  Return 0, TAWPIPE_ECONFIG (bad argument,
- * message in tawpipe_last_error) or TAWPIPE_ERUNTIME (CUDA launch error).  They serve the per-op parity tests. */
+ * message in tawpipe_last_error) or TAWPIPE_ERUNTIME (CUDA launch error).  They serve the per-op parity tests.
+ * Zero rows / tokens (RMSNorm, cross-entropy, embedding) are a no-op: nothing is launched or written. */
 
 /* C[M,N] (+)= Σ_k A(m,k)·B(n,k) (the QKV/O/MLP/head projections and their dgrad/wgrad).
  * A(m,k) = A[m·a_ld + k] if a_kmajor else A[k·a_ld + m]; likewise B(n,k).

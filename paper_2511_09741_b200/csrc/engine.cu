@@ -1755,6 +1755,13 @@ void destroy() {
     if (cm) ncclCommDestroy(cm);
   if (g->world_comm) ncclCommDestroy(g->world_comm);
   for (cudaEvent_t e : g->ev_pool) cudaEventDestroy(e);
+  if (g->inited) {   // the named events build() created
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {g->w_ready[i], g->w_free[i], g->g_ready[i], g->g_free[i]}) cudaEventDestroy(e);
+    for (cudaEvent_t e : {g->evE, g->evF, g->evGF, g->evGE, g->ev_s0, g->ev_s1, g->ev_ws0, g->ev_ws1, g->ev_gs0,
+                          g->ev_gs1})
+      cudaEventDestroy(e);
+  }
   if (g->cs) cudaStreamDestroy(g->cs);
   if (g->ws) cudaStreamDestroy(g->ws);
   if (g->gs) cudaStreamDestroy(g->gs);

@@ -369,7 +369,11 @@ def run_ours(args, c):
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                      "frac": ach / peak, **traffic_for(dom),
                      "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
-                     "share_of_step": dom_ms / ms},
+                     "share_of_step": dom_ms / ms,
+                     "ceiling_note": ("attention backward sits on its shared-memory bound and the forward balances "
+                                      "tensor / MUFU / shared memory at ~2,000 cycles each per unit "
+                                      "(DESIGN.md §5 structural ceilings)" if dom.startswith("causal attention")
+                                      else "CTA-pair GEMM ~99 % tensor-active (DESIGN.md §5)")},
         "kernel_ms": {"gemm": st["gemm_ms"], "attention": st["attn_ms"], "adamw": st["adamw_ms"],
                       "elementwise": st["elementwise_ms"]},
         "gpu_launches": int(round(st["kernel_launches"] * args.steps)),

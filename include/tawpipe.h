@@ -295,6 +295,13 @@ int tawpipe_embed_fwd(int dtype, int B, int S, const int32_t* tokens, int64_t to
 int tawpipe_embed_bwd(int dtype, int B, int S, const int32_t* tokens, int64_t tok_stride, const void* dh, int H,
                       int V, float* dE, void* stream);
 
+/* A non-owner group's rail partial (a8 on the NVLink peer path, "gradients are reduced within the
+ * group, then sent to the owner"): out[i] = wire_dtype( Σ_{m = 0 .. n_src-1, in order} srcs[m][i] ), summed in fp32
+ * (R16).  srcs [n_src] (1..8) device pointers of n fp32 elements each (in the step: the group members' fp32
+ * gradient accumulators, read through IPC peer mappings); out [n] wire_dtype.  n % 4 == 0, pointers 16-byte
+ * aligned.  n == 0 is a no-op. */
+int tawpipe_group_partial(int wire_dtype, int n_src, const float* const* srcs, int64_t n, void* out, void* stream);
+
 /* Fused gradient accumulation + AdamW on one owned stripe (a9; "updates ... applied at the owner";
  * AdamW torch semantics, R1):
  *   g = Σ_{groups gi ascending} ( Σ_{members, in order} srcs[·] )   in fp32 (R16),

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "peer.cuh"
 
 using namespace tp;
 
@@ -264,6 +265,26 @@ int tawpipe_embed_bwd(int dtype, int B, int S, const int32_t* tokens, int64_t to
     TP_CUDA(cudaMallocAsync(&scratch, bytes, s));
     embed_bwd(tokens, tok_stride, B, S, dh, dtype == TAWPIPE_FP32, H, V, dE, scratch, bytes, s);
     TP_CUDA(cudaFreeAsync(scratch, s));
+  });
+}
+
+int tawpipe_group_partial(int wire_dtype, int n_src, const float* const* srcs, int64_t n, void* out, void* stream) {
+  return guarded([&] {
+    check_dtype(wire_dtype);
+    TP_CHECK(n_src >= 1 && n_src <= kMaxPartialSources && srcs && out && n >= 0, TAWPIPE_ECONFIG,
+             "group_partial: 1..8 sources, non-NULL pointers, n >= 0");
+    if (n == 0) return;
+    PartialSources src;
+    for (int i = 0; i < n_src; ++i) {
+      TP_CHECK(srcs[i] && reinterpret_cast<uintptr_t>(srcs[i]) % 16 == 0, TAWPIPE_ECONFIG,
+               "group_partial: sources must be 16-byte aligned");
+      src.p[src.n++] = srcs[i];
+    }
+    TP_CHECK(reinterpret_cast<uintptr_t>(out) % 16 == 0, TAWPIPE_ECONFIG, "group_partial: out must be 16-byte aligned");
+    if (wire_dtype == TAWPIPE_BF16)
+      group_partial<bf16>(src, static_cast<bf16*>(out), n, as_stream(stream));
+    else
+      group_partial<float>(src, static_cast<float*>(out), n, as_stream(stream));
   });
 }
 

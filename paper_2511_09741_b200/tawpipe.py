@@ -89,6 +89,7 @@ def lib():
         "tawpipe_cross_entropy": (i32, [i32, i64, i32, vp, vp, f32, vp, vp]),
         "tawpipe_embed_fwd": (i32, [i32, i32, i32, vp, i64, vp, i32, vp, vp]),
         "tawpipe_embed_bwd": (i32, [i32, i32, i32, vp, i64, vp, i32, i32, vp, vp]),
+        "tawpipe_group_partial": (i32, [i32, i32, vp, i64, vp, vp]),
         "tawpipe_adamw": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
@@ -336,6 +337,12 @@ def embed_fwd(dtype, B, S, tokens, tok_stride, E, H, h, stream=None):
 
 def embed_bwd(dtype, B, S, tokens, tok_stride, dh, H, V, dE, stream=None):
     _check(lib().tawpipe_embed_bwd(dtype, B, S, tokens, tok_stride, dh, H, V, dE, stream))
+
+
+def group_partial(wire_dtype, srcs, n, out, stream=None):
+    """srcs: device pointers of n fp32 elements, summed in list order into out (wire dtype) (tawpipe_group_partial)."""
+    ptrs = (ctypes.c_void_p * len(srcs))(*srcs)
+    _check(lib().tawpipe_group_partial(wire_dtype, len(srcs), ptrs, n, out, stream))
 
 
 def adamw(wire_dtype, groups, master, m, v, wire, n, unit_off=0, no_decay=None, lr=1e-3, beta1=0.9, beta2=0.95,

@@ -240,6 +240,27 @@ def test_embedding_fwd_and_deterministic_bwd_match_oracle(T, dtype, B, S, V, H):
     assert np.all(outs[0][untouched] == 0.25)
 
 
+# ---------------------------------------------------------------------------------------------- rail partial (a8)
+@pytest.mark.parametrize("wdt,G,n", [(F32, 1, 4096), (F32, 2, 1000), (BF, 2, 65536), (BF, 4, 12288), (F32, 8, 4100)])
+def test_group_partial_matches_member_order_sum(T, wdt, G, n):
+    """a8 on the peer path: a non-owner group's rail partial is the members' fp32 stripes summed in member order
+    (R16, oracle/schedule.py reduce: acc = acc + piece, jj ascending), cast once to the wire dtype."""
+    rng = np.random.default_rng(G * 1000 + n)
+    xs = [rng.standard_normal(n).astype(np.float32) * 10.0 ** rng.integers(-3, 1) for _ in range(G)]
+    srcs = [torch.tensor(x).cuda() for x in xs]
+    tdt = torch.float32 if wdt == F32 else torch.bfloat16
+    out = torch.full((n,), 9.0, dtype=tdt, device="cuda")
+    T.group_partial(wdt, [t.data_ptr() for t in srcs], n, out.data_ptr())
+    torch.cuda.synchronize()
+    acc = xs[0].copy()
+    for x in xs[1:]:
+        acc = (acc + x).astype(np.float32)   # fp32, member order: the kernel's exact arithmetic
+    want = torch.tensor(acc).to(tdt)            # one round-to-nearest-even cast to the wire dtype
+    assert torch.equal(out.cpu(), want)
+    ref64 = np.sum(np.stack(xs).astype(np.float64), axis=0)   # the oracle's fp64 sum
+    assert rel(out.float().cpu().numpy(), ref64) < (1e-6 if wdt == F32 else 1e-2)
+
+
 # ---------------------------------------------------------------------------------------------- AdamW (a9)
 ADAM_CASES = [
     # (name, wire dtype, n, groups as lists of source dtypes, eps, wd)

@@ -246,7 +246,7 @@ def test_group_partial_matches_member_order_sum(T, wdt, G, n):
     """a8 on the peer path: a non-owner group's rail partial is the members' fp32 stripes summed in member order
     (R16, oracle/schedule.py reduce: acc = acc + piece, jj ascending), cast once to the wire dtype."""
     rng = np.random.default_rng(G * 1000 + n)
-    xs = [rng.standard_normal(n).astype(np.float32) * 10.0 ** rng.integers(-3, 1) for _ in range(G)]
+    xs = [(rng.standard_normal(n) * 10.0 ** rng.integers(-3, 1)).astype(np.float32) for _ in range(G)]
     srcs = [torch.tensor(x).cuda() for x in xs]
     tdt = torch.float32 if wdt == F32 else torch.bfloat16
     out = torch.full((n,), 9.0, dtype=tdt, device="cuda")

@@ -9,7 +9,8 @@ from helpers import ROOT
 
 
 def header_functions():
-    txt = open(os.path.join(ROOT, "include", "tawpipe.h")).read()
+    with open(os.path.join(ROOT, "include", "tawpipe.h")) as fh:
+        txt = fh.read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(tawpipe_[a-z_0-9]+)\s*\(", txt)))
 

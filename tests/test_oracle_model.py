@@ -122,7 +122,7 @@ def torch_reference_step(params, toks, cfg, n_steps=1):
         loss = total / (N * B * S)
         loss.backward()
         opt.step()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     out = {"embed": P["embed"].detach().numpy(), "head": P["head"].detach().numpy(),
            "final_norm": P["final_norm"].detach().numpy(),
            "layers": [{k: v.detach().numpy() for k, v in lay.items()} for lay in P["layers"]]}
@@ -310,7 +310,9 @@ def test_model_sizes_match_paper():
     """PAPER.md:202 "668 million to 10 billion" (tests/golden/model_sizes.txt)."""
     import os
     path = os.path.join(os.path.dirname(__file__), "golden", "model_sizes.txt")
-    for line in open(path):
+    with open(path) as fh:
+        lines = fh.readlines()
+    for line in lines:
         if line.startswith("#") or not line.strip():
             continue
         L, H, V, n = map(int, line.split())

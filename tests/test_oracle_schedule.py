@@ -124,7 +124,9 @@ def test_validator_catches_each_mutation(mutation, check):
 def _golden():
     path = os.path.join(os.path.dirname(__file__), "golden", "paper_fig3_routes.txt")
     out = {}
-    for line in open(path):
+    with open(path) as fh:
+        lines = fh.readlines()
+    for line in lines:
         if line.startswith("#") or not line.strip():
             continue
         k, *v = line.split()

@@ -89,7 +89,7 @@ def test_bootstrap_unique_id_over_gloo_world2():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()   # no fork of this multi-threaded process
     out = mgr.dict()
     mp.spawn(_uid_worker, args=(2, port, out), nprocs=2, join=True)
     assert len(out) == 2 and out[0] == out[1] and len(bytes.fromhex(out[0])) == 128
